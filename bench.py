@@ -1,0 +1,306 @@
+"""Benchmark of the fused RI scatter-conv layer (the north-star hot path).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload c3|c4|c1] [--impl ours|reference]
+
+One step = one layer forward over one batch (BASELINE.json metric: "RI-conv layer ms &
+effective TFLOP/s").  Default workload C3: 16x16 input, Cin 256 -> Cout 1024, steerable
+R=8 (B=2 bases), subgroup-4 max pooling + argmax + bias, batch 256 per GPU (weak
+scaling: every rank runs its own 256-image shard; no data-path collective).
+
+Rank 0 prints ONE JSON line.  value = whole-job effective TFLOP/s (cuDNN-equivalent
+2*N*H*W*K^2*Cin*Cout*R over all ranks / max-over-ranks device time); ms_per_step = layer
+ms; roofline = algorithmic FLOPs of the fused kernel per launch / its CUDA-event time
+vs the measured bf16 tensor peak; e2e = the same metric through the C-ABI host entry
+point (rc_ri_conv_forward_host) with pinned host buffers, H2D + D2H inside the timed
+region; cpu_baseline = the CPU path on a bounded sample, timed on this host.
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes as C
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+WORKLOADS = {
+    # name: (n per rank, cin, h, w, cout, k, group, R, pool, pool_group, label)
+    "c3": (256, 256, 16, 16, 1024, 3, "steer", 8, "subgroup", 4,
+           "C3: RI conv 16x16x256->1024, steerable R=8 (2 bases), subgroup-4 max+argmax+bias"),
+    "c4": (512, 128, 32, 32, 512, 3, "steer", 16, "subgroup", 4,
+           "C4: RI conv 32x32x128->512, steerable R=16 (4 bases), subgroup-4 max+argmax+bias"),
+    "c1": (32, 64, 8, 8, 256, 3, "single", 1, "none", 1,
+           "C1: single-orientation scatter conv 8x8x64->256"),
+}
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return d.get("bf16_tflops", 1590.0), d.get("hbm_gbs", 6650.0), "measured"
+    return 1590.0, 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled DURING the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines: list[str] = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        rows = []
+        for l in self.lines:
+            f = [x.strip() for x in l.split(",")]
+            if len(f) >= 9:
+                try:
+                    rows.append((float(f[1]), float(f[2]), f[5:9]))
+                except ValueError:
+                    pass
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for _, _, fl in rows for i, v in enumerate(fl) if v.lower() == "active"})
+        return {"sm_mhz": statistics.median(r[0] for r in rows), "sm_max_mhz": max(r[1] for r in rows),
+                "reasons": reasons, "samples": len(rows)}
+
+
+def cpu_reference(wl, threads: int, target_s: float = 12.0):
+    """The CPU path on a bounded image sample (oracle port of the reuse algorithm; for R=1
+    the unmodified reference tiled_scatter_conv).  Returns (eff TFLOP/s, dict)."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import oracle as O
+    n, cin, h, w, cout, k, g, R, pool, pg, _ = wl
+    rng = np.random.default_rng(0)
+    s = 1 / np.sqrt(cin * k * k)
+    kind = "reference" if (g == "single" and O.ref_available()) else "port"
+
+    def run(m):
+        x = rng.uniform(-1, 1, (m, cin, h, w)).astype(np.float32)
+        fx = rng.uniform(-s, s, (cout, cin, k, k)).astype(np.float32)
+        fy = rng.uniform(-s, s, (cout, cin, k, k)).astype(np.float32)
+        t0 = time.perf_counter()
+        if kind == "reference":
+            O.ref_tiled_batch(x, fx, threads, (0, m))
+        else:
+            O.ri_forward(O.Desc(m, cin, h, w, cout, k, g, R, pool, pg), x, fx, fy, nthreads=threads)
+        return time.perf_counter() - t0
+
+    m = threads
+    dt = run(m)  # one image per thread
+    while dt < target_s / 4 and m < n:
+        m = min(n, m * 2)
+        dt = run(m)
+    eff = 2.0 * m * h * w * k * k * cin * cout * R
+    return eff / dt / 1e12, {"cores": threads, "kind": kind,
+                             "sample": f"{m} of {n} images x all {cout} output channels "
+                                       f"({dt:.2f} s), linear in images",
+                             "ms_full_layer_extrapolated": dt * n / m * 1e3}
+
+
+def run_reference(args, wl):
+    rank = int(os.environ.get("RANK", 0))
+    if rank != 0:
+        return
+    threads = os.cpu_count() or 1
+    vals = []
+    info = None
+    for i in range(args.warmup + args.steps):
+        v, info = cpu_reference(wl, threads, target_s=4.0)
+        if i >= args.warmup:
+            vals.append(v)
+    v = statistics.median(vals)
+    n, cin, h, w, cout, k, g, R, pool, pg, label = wl
+    out = {"impl": "reference", "metric": "RI-conv layer effective TFLOP/s", "value": v,
+           "unit": "TFLOP/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+           "ms_per_step": info["ms_full_layer_extrapolated"], "higher_is_better": True,
+           "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+           "config": {"workload": label, "n": n, "orientations": R, "host_threads": threads},
+           "cpu_baseline": {"value": v, "unit": "TFLOP/s", "cores": threads, "kind": info["kind"],
+                            "sample": info["sample"]},
+           "e2e": {"value": v, "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(out), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--workload", default="c3", choices=sorted(WORKLOADS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--precision", default="fp32", choices=["fp32", "bf16x3", "bf16", "auto"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    args = ap.parse_args()
+    wl = WORKLOADS[args.workload]
+    if args.impl == "reference":
+        return run_reference(args, wl)
+
+    import torch
+    import torch.distributed as dist
+    import paper_2512_08888_b200 as P
+    from paper_2512_08888_b200 import _lib
+
+    rank, world = int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1))
+    local = int(os.environ.get("LOCAL_RANK", 0))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    n, cin, h, w, cout, k, g, R, pool, pg, label = wl
+    desc = P.Desc(n, cin, h, w, cout, k, g, R, pool, pg, "scatter", args.precision)
+    gen = torch.Generator(device=dev).manual_seed(1234)  # same weights on every rank
+    s = 1 / np.sqrt(cin * k * k)
+    fx = ((torch.rand((cout, cin, k, k), generator=gen, device=dev) * 2 - 1) * s).contiguous()
+    fy = ((torch.rand((cout, cin, k, k), generator=gen, device=dev) * 2 - 1) * s).contiguous()
+    bias = (torch.rand(cout, generator=gen, device=dev) * 0.2 - 0.1).contiguous()
+    gen.manual_seed(99 + rank)  # each rank its own shard of images
+    x = (torch.rand((n, cin, h, w), generator=gen, device=dev) * 2 - 1).contiguous()
+    bank = P.bank_precompute(desc, fx, fy)
+    ro = desc.out_orientations
+    y = torch.empty((n, cout, ro, h, w), device=dev)
+    am = torch.empty((n, cout, ro, h, w), dtype=torch.uint8, device=dev) if desc.has_argmax else None
+    flush = torch.empty(512 * 1024 * 1024 // 4, device=dev)  # > 126 MB L2
+    stream = torch.cuda.current_stream(dev)
+
+    def step():
+        P.ri_conv_forward(desc, x, bank, bias, out=y, argmax=am)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(args.steps)]
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        for i in range(args.steps):
+            flush.fill_(float(i))  # L2 flush between timed iterations (untimed)
+            ev[i][0].record(stream)
+            step()
+            ev[i][1].record(stream)
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    times = [a.elapsed_time(b) for a, b in ev]  # ms, on the launching stream
+    tot = torch.tensor([sum(times)], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(tot, op=dist.ReduceOp.MAX)
+    ms = tot.item() / args.steps
+    eff_total = desc.eff_flops() * world
+    value = eff_total / (ms * 1e-3) / 1e12
+    alg = desc.alg_flops()
+    achieved = alg / (statistics.mean(times) * 1e-3) / 1e12
+    tpeak, hbm, src = peaks()
+
+    # e2e through the C-ABI host entry point: pinned host buffers, H2D + D2H timed
+    L = _lib.lib()
+    hx = torch.empty((n, cin, h, w), dtype=torch.float32, pin_memory=True)
+    hx.copy_(x)
+    hfx, hfy, hb = (t.cpu().pin_memory() for t in (fx, fy, bias))
+    hy = torch.empty((n, cout, ro, h, w), dtype=torch.float32, pin_memory=True)
+    ha = torch.empty((n, cout, ro, h, w), dtype=torch.uint8, pin_memory=True) if am is not None else None
+    cd = desc.c()
+    pp = lambda t: C.c_void_p(t.data_ptr()) if t is not None else None
+    _lib.check(L.rc_ri_conv_forward_host(C.byref(cd), pp(hx), pp(hfx), pp(hfy), pp(hb), pp(hy), pp(ha), local))
+    if world > 1:
+        dist.barrier()
+    e2e_t = []
+    for _ in range(args.e2e_steps):
+        t0 = time.perf_counter()
+        _lib.check(L.rc_ri_conv_forward_host(C.byref(cd), pp(hx), pp(hfx), pp(hfy), pp(hb), pp(hy), pp(ha), local))
+        e2e_t.append(time.perf_counter() - t0)
+    e2e_s = torch.tensor([statistics.mean(e2e_t)], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(e2e_s, op=dist.ReduceOp.MAX)
+    e2e_val = eff_total / e2e_s.item() / 1e12
+    h2d = hx.numel() * 4 + hfx.numel() * 4 * 2 + hb.numel() * 4
+    d2h = hy.numel() * 4 + (ha.numel() if ha is not None else 0)
+    # parity spot check of the timed output (image 0) against the e2e path
+    ok = torch.equal(y[0].cpu(), hy[0]) if rank == 0 else True
+
+    traffic = None
+    prof = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(prof):
+        tr = json.load(open(prof)).get(f"{args.workload}:{desc.kernel_name()}")
+        traffic = tr
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        v, info = cpu_reference(wl, os.cpu_count() or 1)
+        cpu = {"value": v, "unit": "TFLOP/s", "cores": info["cores"], "kind": info["kind"],
+               "sample": info["sample"], "ms_full_layer_extrapolated": info["ms_full_layer_extrapolated"]}
+    if rank == 0:
+        out = {
+            "metric": "RI-conv layer effective TFLOP/s", "value": value, "unit": "TFLOP/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic (uniform[-1,1) inputs, uniform/sqrt(Cin*K^2) weights, random init)",
+            "config": {"workload": label, "n_per_gpu": n, "c_in": cin, "h": h, "w": w,
+                       "c_out": cout, "k": k, "group": g, "orientations": R, "pool": pool,
+                       "pool_group": pg, "precision": args.precision, "kernel": desc.kernel_name(),
+                       "l2": "flushed between timed iterations (512 MB write)",
+                       "parallelism": f"batch-sharded dp{world}"},
+            "alg_tflops": achieved * 1.0, "eff_tflops_per_gpu": value / world,
+            "roofline": {"bound": "tensor", "achieved": achieved, "peak": tpeak, "unit": "TFLOP/s",
+                         "frac": achieved / tpeak, "traffic": traffic,
+                         "peak_source": f"{src} bf16 dense (MEASURED_PEAKS.json)",
+                         "note": "achieved = algorithmic FLOPs 2*N*H*W*K^2*Cin*Cout*B per launch / "
+                                 "CUDA-event launch time"},
+            "roofline_simt_fp32": {"peak": 74.4, "frac": achieved / 74.4,
+                                   "note": "derived 148 SM x 128 FMA x 2 x 1.965 GHz"},
+            "clocks": clk.summary(),
+            "e2e": {"value": e2e_val, "unit": "TFLOP/s", "h2d_bytes_per_step": int(h2d),
+                    "d2h_bytes_per_step": int(d2h), "ms_per_step": e2e_s.item() * 1e3,
+                    "path": "rc_ri_conv_forward_host (C-ABI, pinned host buffers)"},
+            "gpu_launches": args.steps,
+            "cpu_baseline": cpu,
+            "timed_output_matches_e2e": bool(ok),
+        }
+        print(json.dumps(out), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

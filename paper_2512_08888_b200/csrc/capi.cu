@@ -1,0 +1,339 @@
+// capi.cu -- the extern "C" boundary (include/rotconv_c.h): validation with the
+// reference's messages, bank layout, kernel dispatch, host-buffer drop-in entry points.
+#include <cuda_runtime.h>
+
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "rc_internal.cuh"
+
+namespace rc {
+
+namespace {
+thread_local std::string g_err;
+size_t align256(size_t v) { return (v + 255) & ~size_t(255); }
+}  // namespace
+
+void set_error(const std::string& msg) { g_err = msg; }
+int fail(int status, const std::string& msg) {
+  g_err = msg;
+  return status;
+}
+int cuda_fail(cudaError_t e, const char* where) {
+  g_err = std::string("CUDA error: ") + cudaGetErrorString(e) + " at " + where;
+  return RC_ERR_CUDA;
+}
+
+// Same preconditions (and message strings) as the reference containers and ops:
+// tensor.hpp:38-39, 111-112; scatter_conv.hpp:339-346.
+int validate(const rc_desc& d) {
+  if (d.n < 0) return fail(RC_ERR_INVALID, "ri_conv: batch must be >= 0");
+  if (d.c_in < 1 || d.h < 1 || d.w < 1)
+    return fail(RC_ERR_INVALID, "Tensor3: dimensions must be positive");
+  if (d.c_out < 1) return fail(RC_ERR_INVALID, "FilterBank: channel counts must be positive");
+  if (d.k < 1) return fail(RC_ERR_INVALID, "FilterBank: kernel dims must be >= 1");
+  switch (d.group) {
+    case RC_GROUP_SINGLE:
+      if (d.orientations != 1) return fail(RC_ERR_INVALID, "ri_conv: single group needs 1 orientation");
+      break;
+    case RC_GROUP_P4:
+      if (d.orientations != 4) return fail(RC_ERR_INVALID, "GroupSpec: size must be 4 for p4");
+      break;
+    case RC_GROUP_P4M:
+      if (d.orientations != 8) return fail(RC_ERR_INVALID, "GroupSpec: size must be 8 for p4m");
+      break;
+    case RC_GROUP_STEER:
+      if (d.orientations < 4 || d.orientations % 4 != 0)
+        return fail(RC_ERR_INVALID, "build_orientation_bank: N must be a multiple of 4");
+      break;
+    default: return fail(RC_ERR_INVALID, "ri_conv: unknown group");
+  }
+  if (d.group != RC_GROUP_SINGLE && d.k % 2 == 0)
+    return fail(RC_ERR_INVALID, "transform_kernel: rotation groups need odd square kernels");
+  if (d.orientations > 256) return fail(RC_ERR_INVALID, "ri_conv: at most 256 orientations");
+  switch (d.pool) {
+    case RC_POOL_NONE: case RC_POOL_AVG: case RC_POOL_MAX: break;
+    case RC_POOL_SUBGROUP:
+      if (d.pool_group < 1 || d.orientations % d.pool_group != 0)
+        return fail(RC_ERR_INVALID, "subgroup_pool_max: R not divisible by group_size");
+      break;
+    default: return fail(RC_ERR_INVALID, "ri_conv: unknown pool");
+  }
+  if (d.convention != RC_CONV_SCATTER && d.convention != RC_CONV_RAW)
+    return fail(RC_ERR_INVALID, "ri_conv: unknown convention");
+  if (d.precision < RC_PREC_AUTO || d.precision > RC_PREC_BF16)
+    return fail(RC_ERR_INVALID, "ri_conv: unknown precision");
+  return RC_OK;
+}
+
+BankLayout bank_layout(const rc_desc& d) {
+  BankLayout L{};
+  const size_t per = (size_t)d.c_out * d.c_in * d.k * d.k;
+  const size_t nb = (size_t)num_bases(d);
+  L.bases_off = 0;
+  L.bases_bytes = per * nb * sizeof(float);
+  L.simt_off = align256(L.bases_off + L.bases_bytes);
+  L.simt_bytes = d.k == 3 ? nb * d.c_in * d.c_out * 12 * sizeof(float) : 0;
+  L.tc_off = align256(L.simt_off + L.simt_bytes);
+  L.tc_bytes = 0;
+  L.total = align256(L.tc_off + L.tc_bytes);
+  return L;
+}
+
+void slice_tap_offsets(int k, int convention, TapOffsets* out) {
+  std::memset(out, 0, sizeof(*out));
+  const int kk = k * k, c = k / 2;
+  std::vector<int> cur(kk), nxt(kk);
+  for (int r = 0; r < 4; ++r) {
+    for (int t = 0; t < kk; ++t) cur[t] = t;
+    for (int q = 0; q < r; ++q) {  // tensor.hpp:348-360, one CCW turn
+      for (int i = 0; i < k; ++i)
+        for (int j = 0; j < k; ++j) nxt[i * k + j] = cur[j * k + (k - 1 - i)];
+      cur.swap(nxt);
+    }
+    for (int pos = 0; pos < kk; ++pos) {
+      const int i = pos / k, j = pos % k;
+      // scatter convention reads reverse(rot^r K_b) (scatter_conv.hpp:72-79, 189-193)
+      const int t = convention == RC_CONV_SCATTER ? cur[(k - 1 - i) * k + (k - 1 - j)] : cur[pos];
+      out->di[r][t] = (int8_t)(i - c);
+      out->dj[r][t] = (int8_t)(j - c);
+    }
+  }
+}
+
+}  // namespace rc
+
+using namespace rc;
+
+namespace {
+
+#define RC_CHECK_DESC(d)                                          \
+  do {                                                            \
+    if ((d) == nullptr) return fail(RC_ERR_INVALID, "null desc"); \
+    int st_ = validate(*(d));                                     \
+    if (st_ != RC_OK) return st_;                                 \
+  } while (0)
+
+// per-device cache of staging buffers for the host drop-in entry points
+struct DeviceCache {
+  std::mutex mu;
+  cudaStream_t stream = nullptr;
+  std::vector<std::pair<void*, size_t>> bufs;  // grow-only slots
+  void* get(int slot, size_t bytes) {
+    if ((int)bufs.size() <= slot) bufs.resize(slot + 1, {nullptr, 0});
+    auto& b = bufs[slot];
+    if (b.second < bytes) {
+      if (b.first) cudaFree(b.first);
+      b.first = nullptr;
+      b.second = 0;
+      if (cudaMalloc(&b.first, bytes < 256 ? 256 : bytes) != cudaSuccess) return nullptr;
+      b.second = bytes;
+    }
+    return b.first;
+  }
+};
+DeviceCache g_cache[64];
+
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    cudaGetDevice(&prev);
+    if (prev != dev) cudaSetDevice(dev);
+  }
+  ~DeviceGuard() {
+    int cur;
+    cudaGetDevice(&cur);
+    if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+  }
+};
+
+int dispatch(const rc_desc& d, const float* x, const void* bank, const float* bias, float* y,
+             uint8_t* am, cudaStream_t s, bool dry, const char** name) {
+  if (d.precision == RC_PREC_BF16X3 || d.precision == RC_PREC_BF16)
+    return fail(RC_ERR_UNSUPPORTED, "ri_conv: tensor-core precision not available in this build");
+  int st = launch_simt_k3(d, x, bank, bias, y, am, s, dry, name);
+  if (st != RC_ERR_UNSUPPORTED) return st;
+  if (dry) {
+    if (d.k > kMaxK) return fail(RC_ERR_UNSUPPORTED, "ri_conv: kernel size > 11 unsupported");
+    if (name) *name = "generic";
+    return RC_OK;
+  }
+  st = launch_generic(d, x, bank, bias, y, am, s, name);
+  if (st == RC_ERR_UNSUPPORTED) return fail(st, "ri_conv: kernel size > 11 unsupported");
+  return st;
+}
+
+}  // namespace
+
+extern "C" {
+
+int rc_abi_version(void) { return RC_ABI_VERSION; }
+const char* rc_last_error(void) { return g_err.c_str(); }
+
+int rc_validate(const rc_desc* d) {
+  RC_CHECK_DESC(d);
+  return RC_OK;
+}
+int rc_num_bases(const rc_desc* d) { return d ? num_bases(*d) : 0; }
+int rc_out_orientations(const rc_desc* d) {
+  if (!d || validate(*d) != RC_OK) return 0;
+  return out_orientations(*d);
+}
+
+unsigned long long rc_clipped_writes(int h, int w, int kh, int kw) {
+  const int ch = kh / 2, cw = kw / 2;  // scatter_conv.hpp:94-110
+  unsigned long long total = 0;
+  for (int m = 0; m < kh; ++m) {
+    const int dm = m - ch;
+    const int rows = dm < 0 ? h + dm : h - dm;
+    if (rows <= 0) continue;
+    for (int n = 0; n < kw; ++n) {
+      const int dn = n - cw;
+      const int cols = dn < 0 ? w + dn : w - dn;
+      if (cols > 0) total += (unsigned long long)rows * cols;
+    }
+  }
+  return total;
+}
+
+int rc_analytic_counts(const rc_desc* d, unsigned long long* mults, unsigned long long* adds) {
+  RC_CHECK_DESC(d);
+  const unsigned long long nb = (unsigned long long)num_bases(*d);
+  if (mults)
+    *mults = nb * d->n * (unsigned long long)d->h * d->w * d->k * d->k * d->c_in * d->c_out;
+  if (adds) *adds = nb * d->n * rc_clipped_writes(d->h, d->w, d->k, d->k) * d->c_out;
+  return RC_OK;
+}
+
+int rc_shard_range(int n, int world, int rank, int* begin, int* end) {
+  if (n < 0 || world < 1 || rank < 0 || rank >= world)
+    return fail(RC_ERR_INVALID, "shard_range: need n >= 0, world >= 1, 0 <= rank < world");
+  const int base = n / world, rem = n % world;
+  const int b = rank * base + (rank < rem ? rank : rem);
+  *begin = b;
+  *end = b + base + (rank < rem ? 1 : 0);
+  return RC_OK;
+}
+
+size_t rc_bank_bytes(const rc_desc* d) {
+  if (!d || validate(*d) != RC_OK) return 0;
+  return bank_layout(*d).total;
+}
+
+int rc_bank_precompute(const rc_desc* d, const float* d_w0, const float* d_w1, void* d_bank,
+                       void* stream) {
+  RC_CHECK_DESC(d);
+  if (!d_w0 || !d_bank || (d->group == RC_GROUP_STEER && !d_w1))
+    return fail(RC_ERR_INVALID, "bank_precompute: null pointer");
+  return launch_bank(*d, d_w0, d_w1, d_bank, static_cast<cudaStream_t>(stream));
+}
+
+int rc_orientation_bank(const rc_desc* d, const void* d_bank, float* d_kernels, void* stream) {
+  RC_CHECK_DESC(d);
+  if (!d_bank || !d_kernels) return fail(RC_ERR_INVALID, "orientation_bank: null pointer");
+  return launch_orientation_bank(*d, d_bank, d_kernels, static_cast<cudaStream_t>(stream));
+}
+
+size_t rc_workspace_size(const rc_desc* d) {
+  if (!d || validate(*d) != RC_OK) return 0;
+  return 0;
+}
+
+const char* rc_kernel_name(const rc_desc* d) {
+  if (!d || validate(*d) != RC_OK) return nullptr;
+  const char* name = nullptr;
+  if (dispatch(*d, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, true, &name) != RC_OK)
+    return nullptr;
+  return name;
+}
+
+int rc_ri_conv_forward(const rc_desc* d, const float* d_x, const void* d_bank,
+                       const float* d_bias, float* d_y, uint8_t* d_argmax, void* d_ws,
+                       size_t ws_bytes, void* stream) {
+  RC_CHECK_DESC(d);
+  (void)d_ws;
+  if (ws_bytes < rc_workspace_size(d)) return fail(RC_ERR_WORKSPACE, "ri_conv: workspace too small");
+  if (d->n > 0 && (!d_x || !d_bank || !d_y)) return fail(RC_ERR_INVALID, "ri_conv: null pointer");
+  return dispatch(*d, d_x, d_bank, d_bias, d_y, d_argmax, static_cast<cudaStream_t>(stream),
+                  false, nullptr);
+}
+
+int rc_orientation_pool(int n, int c_out, int r, int h, int w, int pool, int pool_group,
+                        const float* d_f, const float* d_bias, float* d_y, uint8_t* d_argmax,
+                        void* stream) {
+  if (n < 0 || c_out < 1 || r < 1 || h < 1 || w < 1)
+    return fail(RC_ERR_INVALID, "OrientedFeature: dimensions must be positive");
+  if (pool == RC_POOL_SUBGROUP && (pool_group < 1 || r % pool_group != 0))
+    return fail(RC_ERR_INVALID, "subgroup_pool_max: R not divisible by group_size");
+  if (pool < RC_POOL_NONE || pool > RC_POOL_SUBGROUP) return fail(RC_ERR_INVALID, "ri_conv: unknown pool");
+  return launch_pool(n, c_out, r, h, w, pool, pool_group, d_f, d_bias, d_y, d_argmax,
+                     static_cast<cudaStream_t>(stream));
+}
+
+int rc_ri_conv_forward_host(const rc_desc* d, const float* h_x, const float* h_w0,
+                            const float* h_w1, const float* h_bias, float* h_y,
+                            uint8_t* h_argmax, int device) {
+  RC_CHECK_DESC(d);
+  if (device < 0 || device >= 64) return fail(RC_ERR_INVALID, "ri_conv: bad device");
+  if (d->n == 0) return RC_OK;
+  DeviceGuard guard(device);
+  DeviceCache& c = g_cache[device];
+  std::lock_guard<std::mutex> lock(c.mu);
+  if (!c.stream) RC_CUDA(cudaStreamCreateWithFlags(&c.stream, cudaStreamNonBlocking));
+  const size_t xb = (size_t)d->n * d->c_in * d->h * d->w * sizeof(float);
+  const size_t wb = (size_t)d->c_out * d->c_in * d->k * d->k * sizeof(float);
+  const size_t ro = (size_t)out_orientations(*d);
+  const size_t yb = (size_t)d->n * d->c_out * ro * d->h * d->w * sizeof(float);
+  const size_t ab = yb / sizeof(float);
+  const bool has_arg = h_argmax && (d->pool == RC_POOL_MAX || d->pool == RC_POOL_SUBGROUP);
+  void* dx = c.get(0, xb);
+  void* dw0 = c.get(1, wb);
+  void* dw1 = d->group == RC_GROUP_STEER ? c.get(2, wb) : nullptr;
+  void* dbias = h_bias ? c.get(3, d->c_out * sizeof(float)) : nullptr;
+  void* dbank = c.get(4, bank_layout(*d).total);
+  void* dy = c.get(5, yb);
+  void* da = has_arg ? c.get(6, ab) : nullptr;
+  if (!dx || !dw0 || !dbank || !dy || (d->group == RC_GROUP_STEER && !dw1) ||
+      (h_bias && !dbias) || (has_arg && !da))
+    return fail(RC_ERR_CUDA, "ri_conv: device allocation failed");
+  cudaStream_t s = c.stream;
+  RC_CUDA(cudaMemcpyAsync(dx, h_x, xb, cudaMemcpyHostToDevice, s));
+  RC_CUDA(cudaMemcpyAsync(dw0, h_w0, wb, cudaMemcpyHostToDevice, s));
+  if (dw1) RC_CUDA(cudaMemcpyAsync(dw1, h_w1, wb, cudaMemcpyHostToDevice, s));
+  if (dbias) RC_CUDA(cudaMemcpyAsync(dbias, h_bias, d->c_out * sizeof(float), cudaMemcpyHostToDevice, s));
+  int st = launch_bank(*d, (const float*)dw0, (const float*)dw1, dbank, s);
+  if (st != RC_OK) return st;
+  st = dispatch(*d, (const float*)dx, dbank, (const float*)dbias, (float*)dy, (uint8_t*)da, s,
+                false, nullptr);
+  if (st != RC_OK) return st;
+  RC_CUDA(cudaMemcpyAsync(h_y, dy, yb, cudaMemcpyDeviceToHost, s));
+  if (has_arg) RC_CUDA(cudaMemcpyAsync(h_argmax, da, ab, cudaMemcpyDeviceToHost, s));
+  RC_CUDA(cudaStreamSynchronize(s));
+  return RC_OK;
+}
+
+int rc_tiled_scatter_conv_host(const float* h_x, int c_in, int h, int w, const float* h_wt,
+                               int c_out, int in_channels_w, int kh, int kw, int tile_h,
+                               int tile_w, int halo, int workers, int strategy, float* h_y,
+                               unsigned long long* mults, unsigned long long* adds,
+                               unsigned long long* aux_bytes, int device) {
+  (void)strategy;
+  // scatter_conv.hpp:339-346, same order and messages
+  if (c_in != in_channels_w) return fail(RC_ERR_INVALID, "tiled_scatter_conv: channel mismatch");
+  if (kh != kw) return fail(RC_ERR_INVALID, "tiled_scatter_conv: kernel must be square");
+  if (tile_h < 1 || tile_w < 1) return fail(RC_ERR_INVALID, "tiled_scatter_conv: tile dims must be >= 1");
+  if (halo != kh / 2) return fail(RC_ERR_INVALID, "tiled_scatter_conv: invalid halo");
+  if (workers < 1) return fail(RC_ERR_INVALID, "tiled_scatter_conv: workers must be >= 1");
+  rc_desc d{1, c_in, h, w, c_out, kh, RC_GROUP_SINGLE, 1, RC_POOL_NONE, 1, RC_CONV_SCATTER, RC_PREC_FP32};
+  int st = rc_ri_conv_forward_host(&d, h_x, h_wt, nullptr, nullptr, h_y, nullptr, device);
+  if (st != RC_OK) return st;
+  if (mults) *mults = (unsigned long long)h * w * kh * kw * c_in * c_out;  // :361-366
+  if (adds) *adds = rc_clipped_writes(h, w, kh, kw) * c_out;
+  if (aux_bytes) *aux_bytes = rc_workspace_size(&d);
+  return RC_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,74 @@
+// rc_internal.cuh -- shared definitions for the sm_100a kernels behind rotconv_c.h.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+
+#include "rotconv_c.h"
+
+namespace rc {
+
+// ---- error plumbing (thread-local message, rotconv_c.h "Conventions") ----------
+void set_error(const std::string& msg);
+int fail(int status, const std::string& msg);
+int cuda_fail(cudaError_t e, const char* where);
+#define RC_CUDA(call)                                            \
+  do {                                                           \
+    cudaError_t e_ = (call);                                     \
+    if (e_ != cudaSuccess) return ::rc::cuda_fail(e_, #call);    \
+  } while (0)
+
+// ---- descriptor helpers ----------------------------------------------------------
+inline int num_bases(const rc_desc& d) {
+  return d.group == RC_GROUP_P4M ? 2 : (d.group == RC_GROUP_STEER ? d.orientations / 4 : 1);
+}
+inline int rot_per_base(const rc_desc& d) { return d.group == RC_GROUP_SINGLE ? 1 : 4; }
+inline int out_orientations(const rc_desc& d) {
+  const int R = num_bases(d) * rot_per_base(d);
+  if (d.pool == RC_POOL_NONE) return R;
+  if (d.pool == RC_POOL_SUBGROUP) return R / d.pool_group;
+  return 1;
+}
+// group size of the pooling fold: every `g` consecutive orientations reduce to one
+inline int pool_fold(const rc_desc& d) {
+  const int R = num_bases(d) * rot_per_base(d);
+  if (d.pool == RC_POOL_NONE) return 1;
+  if (d.pool == RC_POOL_SUBGROUP) return d.pool_group;
+  return R;
+}
+int validate(const rc_desc& d);  // RC_OK or RC_ERR_INVALID + message
+
+// ---- bank layout (rc_bank_bytes) ---------------------------------------------------
+struct BankLayout {
+  size_t bases_off, bases_bytes;  // fp32 [B][Cout][Cin][K][K]
+  size_t simt_off, simt_bytes;    // K==3 SIMT operand: fp32 [B][Cin][Cout][12] (9 taps + 3 pad)
+  size_t tc_off, tc_bytes;        // tcgen05 packed operands (0 if none)
+  size_t total;
+};
+BankLayout bank_layout(const rc_desc& d);
+
+// ---- slice index maps (convention P1) ---------------------------------------------
+// For rotation r of a base kernel K_b, the slice kernel read at gather position
+// (i, j) is base tap map[i*k+j] (rc_oracle.c rco_slice_tap_map restates the same).
+constexpr int kMaxK = 11;
+struct TapOffsets {  // per rotation r < 4 and base tap t: gather offset (di, dj)
+  int8_t di[4][kMaxK * kMaxK];
+  int8_t dj[4][kMaxK * kMaxK];
+};
+void slice_tap_offsets(int k, int convention, TapOffsets* out);
+
+// ---- kernel launchers ----------------------------------------------------------------
+int launch_bank(const rc_desc& d, const float* w0, const float* w1, void* bank,
+                cudaStream_t s);
+int launch_orientation_bank(const rc_desc& d, const void* bank, float* out, cudaStream_t s);
+// returns RC_ERR_UNSUPPORTED if the SIMT K=3 fast kernel cannot handle d
+int launch_simt_k3(const rc_desc& d, const float* x, const void* bank, const float* bias,
+                   float* y, uint8_t* argmax, cudaStream_t s, bool dry_run, const char** name);
+int launch_generic(const rc_desc& d, const float* x, const void* bank, const float* bias,
+                   float* y, uint8_t* argmax, cudaStream_t s, const char** name);
+int launch_pool(int n, int c_out, int r, int h, int w, int pool, int g, const float* f,
+                const float* bias, float* y, uint8_t* argmax, cudaStream_t s);
+
+}  // namespace rc
