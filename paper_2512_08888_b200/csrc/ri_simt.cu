@@ -255,11 +255,19 @@ struct SimtK3 {
 
   template <int P>
   __device__ void step(int b, int q, int& gi, int total) {
-    // slot (P+1)%3 held output row q-2 (finalised last step); it now receives row q+1
+    // slot (P+1)%3 held output row q-2 (finalised last step); it now receives row q+1.
+    // At q == 0 (start of a base) slot P (row 0) is fresh too; slot (P+2)%3 collects the
+    // clipped row -1 and is zeroed before reuse at q == 1.
 #pragma unroll
     for (int r = 0; r < RPB; ++r)
 #pragma unroll
       for (int j = 0; j < SW; ++j) Y[(P + 1) % 3][r][j] = 0.f;
+    if (P == 0 && q == 0) {
+#pragma unroll
+      for (int r = 0; r < RPB; ++r)
+#pragma unroll
+        for (int j = 0; j < SW; ++j) Y[0][r][j] = 0.f;
+    }
 #pragma unroll
     for (int t = 0; t < 9; ++t)
 #pragma unroll

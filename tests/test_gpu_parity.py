@@ -2,7 +2,9 @@
 
 Tolerances (FP32 path, stated here as the contract):
   * dyadic inputs (values k/4): bit-exact values AND argmax (every product and partial
-    sum is exactly representable, so summation order cannot matter);
+    sum is exactly representable, so summation order cannot matter) -- for single, p4,
+    p4m and steer N=4; steered bases at 2*pi*b/N (b >= 1) are irrational and fall back
+    to the random-input tolerance;
   * random inputs: normwise max|dy| / max|y| <= 2e-6 and, where the oracle's top-2
     orientation gap exceeds 1e-4 * max|y|, argmax identical.
 """
@@ -72,6 +74,12 @@ def test_dyadic_bitexact(O, dev, cfg, convention):
     bias = dyadic(rng, d.c_out)
     y_ref, a_ref = O.ri_forward(d, x, w0, w1, bias)
     y, a, kname = gpu_forward(P, d, x, w0, w1, bias)
+    if d.group == "steer" and d.orientations > 4:
+        # bases at theta = 2*pi*b/N, b >= 1, carry irrational sin/cos coefficients: the
+        # operands are no longer dyadic, so only the FP32 tolerance applies
+        err = np.abs(y.astype(np.float64) - y_ref).max() / np.abs(y_ref).max()
+        assert err <= NORMWISE_TOL, f"{kname}: normwise {err:.3e}"
+        return
     assert np.array_equal(y, y_ref), f"{kname}: max|dy|={np.abs(y - y_ref).max()}"
     if a_ref is not None:
         assert np.array_equal(a, a_ref), f"{kname}: argmax mismatches {(a != a_ref).sum()}"
@@ -166,19 +174,23 @@ def test_golden_fixtures_on_gpu(O, dev, golden):
         g = list(O.GROUPS)[gi]
         d = O.Desc(1, int(cin), int(h), int(w), int(cout), 3, g, int(R))
         y, _, _ = gpu_forward(P, d, golden[key + "_x"][None], golden[key + "_w0"], golden[key + "_w1"])
-        assert np.array_equal(y[0], golden[key + "_f"]), key
+        ref = golden[key + "_f"]
+        if g == "steer" and R > 4:  # irrational steering coefficients: FP32 tolerance
+            assert np.abs(y[0] - ref).max() <= NORMWISE_TOL * np.abs(ref).max(), key
+        else:
+            assert np.array_equal(y[0], ref), key
 
 
 def test_host_entry_point_matches_device_path(O, dev):
     """rc_ri_conv_forward_host (the e2e drop-in) == device path == oracle (dyadic)."""
     from paper_2512_08888_b200 import _lib
     rng = np.random.default_rng(5)
-    d = O.Desc(3, 8, 16, 16, 24, 3, "steer", 8, "subgroup", 4)
+    d = O.Desc(3, 8, 16, 16, 24, 3, "p4m", 8, "subgroup", 4)
     x = dyadic(rng, (3, 8, 16, 16))
     fx, fy, b = dyadic(rng, (24, 8, 3, 3)), dyadic(rng, (24, 8, 3, 3)), dyadic(rng, 24)
     y = np.zeros((3, 24, 2, 16, 16), np.float32)
     a = np.zeros((3, 24, 2, 16, 16), np.uint8)
-    cd = _lib.rc_desc(3, 8, 16, 16, 24, 3, 3, 8, 3, 4, 0, 1)
+    cd = _lib.rc_desc(3, 8, 16, 16, 24, 3, 2, 8, 3, 4, 0, 1)
     p = lambda arr: C.c_void_p(arr.ctypes.data)
     _lib.check(_lib.lib().rc_ri_conv_forward_host(C.byref(cd), p(x), p(fx), p(fy), p(b), p(y), p(a), 0))
     yr, ar = O.ri_forward(d, x, fx, fy, b)
