@@ -66,7 +66,7 @@ class ClockSampler:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
+                 "--format=csv,noheader,nounits", "-lms", "10"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
@@ -247,7 +247,7 @@ def main():
     if world > 1:
         dist.barrier()
     e2e_t = []
-    for _ in range(args.e2e_steps):
+    for _ in range(max(1, args.e2e_steps)):
         t0 = time.perf_counter()
         _lib.check(L.rc_ri_conv_forward_host(C.byref(cd), pp(hx), pp(hfx), pp(hfy), pp(hb), pp(hy), pp(ha), local))
         e2e_t.append(time.perf_counter() - t0)

@@ -101,6 +101,9 @@ int launch_bank(const rc_desc& d, const float* w0, const float* w1, void* bank, 
       w0, d.group == RC_GROUP_STEER ? w1 : w0, reinterpret_cast<float*>(base + L.bases_off), simt,
       nb, d.c_out, d.c_in, d.k, d.group, c);
   RC_CUDA(cudaGetLastError());
+  if (L.tc_bytes)  // tcgen05 operand tiles (bf16 hi/lo, SW128) from the fp32 bases
+    return launch_tc_wpack(d, reinterpret_cast<const float*>(base + L.bases_off),
+                           reinterpret_cast<uint8_t*>(base + L.tc_off), s);
   return RC_OK;
 }
 

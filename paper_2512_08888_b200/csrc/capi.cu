@@ -78,7 +78,7 @@ BankLayout bank_layout(const rc_desc& d) {
   L.simt_off = align256(L.bases_off + L.bases_bytes);
   L.simt_bytes = d.k == 3 ? nb * d.c_in * d.c_out * 12 * sizeof(float) : 0;
   L.tc_off = align256(L.simt_off + L.simt_bytes);
-  L.tc_bytes = 0;
+  L.tc_bytes = tc_bank_bytes(d);
   L.total = align256(L.tc_off + L.tc_bytes);
   return L;
 }
@@ -150,10 +150,18 @@ struct DeviceGuard {
   }
 };
 
+// precision FP32 -> CUDA-core kernels; BF16 / BF16X3 -> tcgen05 kernel or UNSUPPORTED
+// (never silently a different arithmetic); AUTO -> tensor cores where supported.
 int dispatch(const rc_desc& d, const float* x, const void* bank, const float* bias, float* y,
-             uint8_t* am, cudaStream_t s, bool dry, const char** name) {
-  if (d.precision == RC_PREC_BF16X3 || d.precision == RC_PREC_BF16)
-    return fail(RC_ERR_UNSUPPORTED, "ri_conv: tensor-core precision not available in this build");
+             uint8_t* am, void* ws, size_t ws_bytes, cudaStream_t s, bool dry, const char** name) {
+  if (d.precision == RC_PREC_BF16X3 || d.precision == RC_PREC_BF16 || d.precision == RC_PREC_AUTO) {
+    int st = launch_tc(d, x, bank, bias, y, am, ws, ws_bytes, s, dry, name);
+    if (st != RC_ERR_UNSUPPORTED || d.precision != RC_PREC_AUTO) {
+      if (st == RC_ERR_UNSUPPORTED)
+        return fail(st, "ri_conv: no tensor-core kernel for this shape (K=3, W=16, rotation group)");
+      return st;
+    }
+  }
   int st = launch_simt_k3(d, x, bank, bias, y, am, s, dry, name);
   if (st != RC_ERR_UNSUPPORTED) return st;
   if (dry) {
@@ -239,13 +247,13 @@ int rc_orientation_bank(const rc_desc* d, const void* d_bank, float* d_kernels, 
 
 size_t rc_workspace_size(const rc_desc* d) {
   if (!d || validate(*d) != RC_OK) return 0;
-  return 0;
+  return tc_workspace_bytes(*d);
 }
 
 const char* rc_kernel_name(const rc_desc* d) {
   if (!d || validate(*d) != RC_OK) return nullptr;
   const char* name = nullptr;
-  if (dispatch(*d, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, true, &name) != RC_OK)
+  if (dispatch(*d, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, 0, nullptr, true, &name) != RC_OK)
     return nullptr;
   return name;
 }
@@ -257,7 +265,7 @@ int rc_ri_conv_forward(const rc_desc* d, const float* d_x, const void* d_bank,
   (void)d_ws;
   if (ws_bytes < rc_workspace_size(d)) return fail(RC_ERR_WORKSPACE, "ri_conv: workspace too small");
   if (d->n > 0 && (!d_x || !d_bank || !d_y)) return fail(RC_ERR_INVALID, "ri_conv: null pointer");
-  return dispatch(*d, d_x, d_bank, d_bias, d_y, d_argmax, static_cast<cudaStream_t>(stream),
+  return dispatch(*d, d_x, d_bank, d_bias, d_y, d_argmax, d_ws, ws_bytes, static_cast<cudaStream_t>(stream),
                   false, nullptr);
 }
 
@@ -296,8 +304,10 @@ int rc_ri_conv_forward_host(const rc_desc* d, const float* h_x, const float* h_w
   void* dbank = c.get(4, bank_layout(*d).total);
   void* dy = c.get(5, yb);
   void* da = has_arg ? c.get(6, ab) : nullptr;
+  const size_t wsb = tc_workspace_bytes(*d);
+  void* dws = wsb ? c.get(7, wsb) : nullptr;
   if (!dx || !dw0 || !dbank || !dy || (d->group == RC_GROUP_STEER && !dw1) ||
-      (h_bias && !dbias) || (has_arg && !da))
+      (h_bias && !dbias) || (has_arg && !da) || (wsb && !dws))
     return fail(RC_ERR_CUDA, "ri_conv: device allocation failed");
   cudaStream_t s = c.stream;
   RC_CUDA(cudaMemcpyAsync(dx, h_x, xb, cudaMemcpyHostToDevice, s));
@@ -306,7 +316,7 @@ int rc_ri_conv_forward_host(const rc_desc* d, const float* h_x, const float* h_w
   if (dbias) RC_CUDA(cudaMemcpyAsync(dbias, h_bias, d->c_out * sizeof(float), cudaMemcpyHostToDevice, s));
   int st = launch_bank(*d, (const float*)dw0, (const float*)dw1, dbank, s);
   if (st != RC_OK) return st;
-  st = dispatch(*d, (const float*)dx, dbank, (const float*)dbias, (float*)dy, (uint8_t*)da, s,
+  st = dispatch(*d, (const float*)dx, dbank, (const float*)dbias, (float*)dy, (uint8_t*)da, dws, wsb, s,
                 false, nullptr);
   if (st != RC_OK) return st;
   RC_CUDA(cudaMemcpyAsync(h_y, dy, yb, cudaMemcpyDeviceToHost, s));

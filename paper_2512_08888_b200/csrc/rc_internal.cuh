@@ -72,3 +72,13 @@ int launch_pool(int n, int c_out, int r, int h, int w, int pool, int g, const fl
                 const float* bias, float* y, uint8_t* argmax, cudaStream_t s);
 
 }  // namespace rc
+
+namespace rc {
+// tensor-core path (ri_tc.cu)
+bool tc_supported(const rc_desc& d);
+size_t tc_bank_bytes(const rc_desc& d);
+size_t tc_workspace_bytes(const rc_desc& d);
+int launch_tc_wpack(const rc_desc& d, const float* bases, uint8_t* tc_section, cudaStream_t s);
+int launch_tc(const rc_desc& d, const float* x, const void* bank, const float* bias, float* y, uint8_t* am,
+              void* ws, size_t ws_bytes, cudaStream_t s, bool dry_run, const char** name);
+}  // namespace rc

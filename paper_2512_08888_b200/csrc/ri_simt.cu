@@ -21,38 +21,13 @@
 // a fixed order, so dyadic inputs reproduce the oracle bit-for-bit (tests/test_gpu_parity).
 #include <algorithm>
 
+#include "k3_tables.cuh"
 #include "rc_internal.cuh"
 
 namespace rc {
 namespace {
 
 constexpr int CC = 16;  // input channels per shared-memory stage
-
-struct K3Tables {
-  int di[4][9];
-  int dj[4][9];
-};
-
-// rco_slice_tap_map (rc_oracle.c) for K = 3 as a constant expression: rot90^r of the
-// tap-id plane (tensor.hpp:348-360), reversed for the scatter convention.
-__host__ __device__ constexpr K3Tables make_k3(int conv) {
-  K3Tables T{};
-  for (int r = 0; r < 4; ++r) {
-    int cur[9] = {0, 1, 2, 3, 4, 5, 6, 7, 8};
-    for (int q = 0; q < r; ++q) {
-      int nxt[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
-      for (int i = 0; i < 3; ++i)
-        for (int j = 0; j < 3; ++j) nxt[i * 3 + j] = cur[j * 3 + (2 - i)];
-      for (int t = 0; t < 9; ++t) cur[t] = nxt[t];
-    }
-    for (int pos = 0; pos < 9; ++pos) {
-      const int t = conv == 0 ? cur[8 - pos] : cur[pos];
-      T.di[r][t] = pos / 3 - 1;
-      T.dj[r][t] = pos % 3 - 1;
-    }
-  }
-  return T;
-}
 
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool valid) {
   const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));

@@ -1,0 +1,117 @@
+"""Tensor-core (tcgen05) path parity vs the CPU oracle.
+
+Tolerances, stated per arithmetic:
+  * dyadic inputs (k/4) are exact in bf16 (hi part; lo part 0), so both "bf16" and
+    "bf16x3" reproduce the oracle bit-for-bit (values and argmax) for p4 / p4m;
+  * random inputs, normwise max|dy|/max|y|:  bf16x3 <= 3e-5,  bf16 <= 1e-2.
+"""
+import numpy as np
+import pytest
+import torch
+
+from conftest import dyadic
+
+pytestmark = pytest.mark.gpu
+
+TOL = {"bf16x3": 3e-5, "bf16": 1e-2}
+
+
+def run(P, d, x, w0, w1, bias, precision, dev):
+    t = lambda a: None if a is None else torch.from_numpy(np.ascontiguousarray(a)).to(dev)
+    desc = P.Desc(d.n, d.c_in, d.h, d.w, d.c_out, d.k, d.group, d.orientations, d.pool, d.pool_group,
+                  d.convention, precision)
+    assert desc.kernel_name().startswith("tc_"), desc.kernel_name()
+    bank = P.bank_precompute(desc, t(w0), t(w1))
+    y, a = P.ri_conv_forward(desc, t(x), bank, t(bias))
+    torch.cuda.synchronize()
+    y = y.cpu().numpy()
+    a = a.cpu().numpy() if a is not None else None
+    if d.pool in ("avg", "max"):
+        y = y[:, :, 0]
+        a = a[:, :, 0] if a is not None else None
+    return y, a
+
+
+TC_CONFIGS = [
+    # (n, cin, h, cout, group, R, pool, g, convention)
+    (2, 64, 16, 128, "p4", 4, "subgroup", 4, "scatter"),
+    (3, 16, 16, 128, "p4m", 8, "subgroup", 4, "scatter"),
+    (2, 100, 13, 200, "p4m", 8, "max", 8, "scatter"),
+    (2, 64, 4, 128, "p4", 4, "none", 4, "scatter"),
+    (1, 32, 1, 128, "p4", 4, "avg", 4, "raw"),
+    (2, 256, 16, 256, "p4m", 8, "subgroup", 2, "scatter"),
+    (2, 48, 9, 130, "p4m", 8, "subgroup", 1, "raw"),
+    (2, 64, 16, 128, "p4m", 8, "avg", 4, "scatter"),
+]
+
+
+@pytest.mark.parametrize("precision", ["bf16", "bf16x3"])
+@pytest.mark.parametrize("cfg", TC_CONFIGS, ids=lambda c: "-".join(map(str, c)))
+def test_tc_dyadic_bitexact(O, dev, cfg, precision):
+    import paper_2512_08888_b200 as P
+    n, cin, h, cout, g, R, pool, pg, conv = cfg
+    d = O.Desc(n, cin, h, 16, cout, 3, g, R, pool, pg, conv)
+    rng = np.random.default_rng(abs(hash(cfg)) % 2**32)
+    x = dyadic(rng, (n, cin, h, 16))
+    w0 = dyadic(rng, (cout, cin, 3, 3))
+    bias = dyadic(rng, cout)
+    y_ref, a_ref = O.ri_forward(d, x, w0, None, bias)
+    y, a = run(P, d, x, w0, None, bias, precision, dev)
+    assert np.array_equal(y, y_ref), f"max|dy| = {np.abs(y - y_ref).max()}"
+    if a_ref is not None:
+        assert np.array_equal(a, a_ref), f"argmax mismatches {(a != a_ref).sum()}"
+
+
+@pytest.mark.parametrize("precision", ["bf16", "bf16x3"])
+@pytest.mark.parametrize("cfg", [(2, 256, 16, 256, "steer", 8, "subgroup", 4),
+                                 (2, 128, 16, 128, "steer", 16, "subgroup", 4),
+                                 (2, 64, 11, 128, "steer", 12, "max", 12),
+                                 (2, 96, 16, 192, "p4m", 8, "subgroup", 4)],
+                         ids=lambda c: "-".join(map(str, c)))
+def test_tc_random_tolerance(O, dev, cfg, precision):
+    import paper_2512_08888_b200 as P
+    n, cin, h, cout, g, R, pool, pg = cfg
+    d = O.Desc(n, cin, h, 16, cout, 3, g, R, pool, pg)
+    rng = np.random.default_rng(7 + abs(hash(cfg)) % 2**31)
+    x = rng.uniform(-1, 1, (n, cin, h, 16)).astype(np.float32)
+    s = 1 / np.sqrt(cin * 9)
+    w0 = rng.uniform(-s, s, (cout, cin, 3, 3)).astype(np.float32)
+    w1 = rng.uniform(-s, s, (cout, cin, 3, 3)).astype(np.float32)
+    bias = rng.uniform(-0.1, 0.1, cout).astype(np.float32)
+    y_ref, a_ref = O.ri_forward(d, x, w0, w1, bias)
+    y, a = run(P, d, x, w0, w1, bias, precision, dev)
+    err = np.abs(y.astype(np.float64) - y_ref).max() / np.abs(y_ref).max()
+    assert err <= TOL[precision], f"normwise {err:.3e}"
+    if precision == "bf16x3" and a_ref is not None:
+        dn = O.Desc(n, cin, h, 16, cout, 3, g, R, "none")
+        f, _ = O.ri_forward(dn, x, w0, w1)
+        gg = R if pool == "max" else pg
+        blk = np.sort(f.reshape(n, cout, R // gg, gg, h, 16), axis=3)
+        gap = blk[:, :, :, -1] - blk[:, :, :, -2]
+        if pool == "max":
+            gap = gap[:, :, 0]
+        safe = gap > 1e-3 * np.abs(y_ref).max()
+        assert np.array_equal(a[safe], a_ref[safe])
+
+
+def test_tc_matches_simt_on_c3_shape_subset(O, dev):
+    """C3 layer shape (256 -> 1024, steer R=8, subgroup-4) on 8 images: bf16x3 vs the
+    FP32 CUDA-core kernel, normwise, plus determinism."""
+    import paper_2512_08888_b200 as P
+    g = torch.Generator(device=dev).manual_seed(3)
+    n, cin, cout = 8, 256, 1024
+    x = torch.rand((n, cin, 16, 16), generator=g, device=dev) * 2 - 1
+    s = 1 / np.sqrt(cin * 9)
+    fx = (torch.rand((cout, cin, 3, 3), generator=g, device=dev) * 2 - 1) * s
+    fy = (torch.rand((cout, cin, 3, 3), generator=g, device=dev) * 2 - 1) * s
+    outs = {}
+    for prec in ("fp32", "bf16x3", "bf16x3"):
+        d = P.Desc(n, cin, 16, 16, cout, 3, "steer", 8, "subgroup", 4, "scatter", prec)
+        bank = P.bank_precompute(d, fx, fy)
+        y, a = P.ri_conv_forward(d, x, bank)
+        outs.setdefault(prec, []).append((y.clone(), a.clone()))
+    y32 = outs["fp32"][0][0]
+    y3 = outs["bf16x3"][0][0]
+    assert torch.equal(outs["bf16x3"][0][0], outs["bf16x3"][1][0])
+    err = ((y3 - y32).abs().max() / y32.abs().max()).item()
+    assert err <= TOL["bf16x3"], err
