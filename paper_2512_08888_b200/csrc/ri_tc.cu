@@ -2,26 +2,28 @@
 //
 // Same math as ri_simt.cu (convention P1), with the channel contraction on
 // the 5th-generation tensor cores:
-//   Z_t[co, px] = sum_ci W_{b,t}[co, ci] * X[ci, px]      tcgen05.mma kind::f16, M=128 co,
-//                                                         N=64 px (one 4-row band), FP32 in TMEM
-//   Y_{b,r}(p) += Z_t(p + delta_{r,t})                    CUDA-core epilogue, reuse over r
+//   Z_t[co, px] = sum_ci W_{b,t}[co, ci] * X[ci, px]      tcgen05.mma kind::f16, M = 128 co,
+//                                                         N = 96 px, FP32 accumulators in TMEM
+//   Y_{b,r}(p) += Z_t(p + delta_{r,t})                    CUDA-core epilogue, reused by all 4 r
 // precision "bf16"  : one product, bf16 operands;
-// precision "bf16x3": operands split hi+lo (bf16 each), hi*hi + hi*lo + lo*hi, FP32-class.
+// precision "bf16x3": operands split hi + lo (bf16 each); hi*hi + hi*lo + lo*hi, FP32-class.
 //
-// Layout / dataflow per persistent CTA (1 CTA per SM, 10 warps):
-//   warp 0  producer   : 1-D bulk copies (TMA engine) of pre-packed SW128 tiles:
-//                        X band [64 px x 64 ci] per ci-chunk (double-buffered per band),
-//                        W tap tiles [128 co x 64 ci] through a ring of W_STAGES stages.
-//   warp 1  MMA issuer : one elected thread; per (base, band, tap) accumulates K into one
-//                        of two 64-column TMEM buffers, commits to mbarriers.
-//   warps 2-9 epilogue : TMEM lane = output channel (co); every thread owns full 16-px image
-//                        rows, so the spatial scatter is register indexing.  Two warps per
-//                        lane quadrant split the band's 4 output rows (2 each); 128 fp32 Y
-//                        registers per thread (2 rows x 4 rotations x 16 px).
-// Bands lag by one row: band k computes input rows [4k, 4k+4) and completes output rows
-// [4k-1, 4k+3); the two input rows above the band (4k-2, 4k-1) are kept in TMEM
-// ("kept slots", 2 rows x 9 taps) by the h=0 epilogue warps, so no row is ever
-// recomputed.  TMEM: D buffers cols [0,128), kept slots [128, 416).
+// Work item = (co tile of 128, image); per base b the image is swept in bands of 4 output
+// rows.  A band's MMA covers the 6 input rows [4k-1, 4k+5) (one halo row above and below,
+// recomputed: 1.5x the MMA work, no cross-band state in TMEM and no cross-warp races).
+//
+// Persistent CTA (1 per SM), 20 warps:
+//   warp 0      producer  : 1-D bulk copies (TMA engine) of pre-packed SW128 tiles: the X
+//                           band (NC tiles of [96 px x 64 ci]) and, per stage, spc ci-chunks of
+//                           one tap's weights [128 co x 64 ci] (>= 32 KB per copy).
+//   warp 1      MMA       : elected lane issues tcgen05.mma (M=128, N=96, K=16) into one of
+//                           NDB TMEM buffers per (base, band, tap) and commits to mbarriers.
+//   warps 2, 3  idle (complete the producer warpgroup for setmaxnreg).
+//   warps 4-19  epilogue  : TMEM lane = output channel co.  The 4 warps of a lane quadrant
+//                           split the band into (2 output rows) x (8 columns); each thread
+//                           holds Y[2 rows][4 rotations][8 px] = 64 fp32 registers, reads
+//                           the 4 input rows it needs (10 columns incl. halo) straight from
+//                           TMEM, scatters with compile-time offsets, then pools + stores.
 // Pooling / argmax / bias epilogue identical to the SIMT kernel; 128-bit stores.
 #include <cuda_bf16.h>
 
@@ -34,86 +36,91 @@ namespace {
 
 using namespace tc;
 
-constexpr int TW = 16;        // image width handled by this kernel
-constexpr int BAND_ROWS = 4;  // input rows per band
-constexpr int BAND_PX = 64;   // = N of the MMA
-constexpr int KC = 64;        // ci per chunk (one 128-byte swizzle row of bf16)
-constexpr int XTILE = BAND_PX * KC * 2;  // 8 KB
+constexpr int TW = 16;                  // image width handled by this kernel
+constexpr int OUT_ROWS = 4;             // output rows per band
+constexpr int IN_ROWS = OUT_ROWS + 2;   // input rows per band (halo above and below)
+constexpr int BAND_PX = IN_ROWS * TW;   // 96 = N of the MMA
+constexpr int KC = 64;                  // ci per chunk (one 128-byte swizzle row of bf16)
+constexpr int XTILE = BAND_PX * KC * 2;  // 12 KB
 constexpr int WTILE = 128 * KC * 2;      // 16 KB
-constexpr int NUM_EPI = 8;
-constexpr int THREADS = 32 * (2 + NUM_EPI);
-constexpr uint32_t KEPT0 = 128;
+constexpr int NUM_EPI = 16;              // epilogue warps (4 warpgroups)
+constexpr int EPI_WARP0 = 4;             // warps 0-3: producer warpgroup (TMA, MMA, 2 idle)
+constexpr int THREADS = 32 * (EPI_WARP0 + NUM_EPI);
+constexpr int REGS_PRODUCER = 40;        // setmaxnreg budgets: 20 warps x 96 at launch
+constexpr int REGS_EPILOGUE = 104;
+constexpr int NDB = 4;                   // TMEM accumulator buffers (MMA <-> epilogue)
+constexpr uint32_t D0 = 16;              // D buffers from column 16: the 1-column-left halo
+                                         // load of a row stays inside the allocation
+constexpr int XH = 8;                    // output columns per epilogue thread
+constexpr int ZW = XH + 2;               // loaded columns incl. the halo on both sides
+// TMEM columns: 16 + 4 * 96 = 400 <= 512
 
 struct TcParams {
-  const uint8_t* xh;  // packed X tiles [n][band][chunk] (hi), 8 KB each
+  const uint8_t* xh;  // packed X tiles [n][band][chunk] (hi), 12 KB each
   const uint8_t* xl;  // lo plane (3-pass) or null
-  const uint8_t* wh;  // packed W tiles [b][ct][t][chunk] (hi), 16 KB each
-  const uint8_t* wl;  // lo plane
+  const uint8_t* w;   // packed W tiles: bf16x3 [b][ct][t][chunk][part], bf16 [b][ct][t][chunk]
   const float* bias;
   float* y;
   uint8_t* am;
-  int N, H, Cout, NB, NBK, NC, NCT, pool, gf, RO, passes, w_stages, items;
+  int N, H, Cout, NB, NBK, NC, NCT, pool, gf, RO, passes, w_stages, spc, x_bufs, items;
+  float inv_r;  // 1/R for average pooling (R a power of two)
 };
 
-__device__ __forceinline__ void tmem_st16(uint32_t taddr, const float (&v)[16]) {
-  asm volatile(
-      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};\n" ::"r"(
-          taddr),
-      "r"(__float_as_uint(v[0])), "r"(__float_as_uint(v[1])), "r"(__float_as_uint(v[2])),
-      "r"(__float_as_uint(v[3])), "r"(__float_as_uint(v[4])), "r"(__float_as_uint(v[5])),
-      "r"(__float_as_uint(v[6])), "r"(__float_as_uint(v[7])), "r"(__float_as_uint(v[8])),
-      "r"(__float_as_uint(v[9])), "r"(__float_as_uint(v[10])), "r"(__float_as_uint(v[11])),
-      "r"(__float_as_uint(v[12])), "r"(__float_as_uint(v[13])), "r"(__float_as_uint(v[14])),
-      "r"(__float_as_uint(v[15])));
-}
-__device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory"); }
-
-__device__ __forceinline__ void store16(float* dst, const float (&v)[16]) {
-  float4* d4 = reinterpret_cast<float4*>(dst);
+// ---- TMEM -> registers ----------------------------------------------------------------
+__device__ __forceinline__ void tmem_ld8(uint32_t taddr, float* v) {
+  uint32_t r[8];
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];\n"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+               : "r"(taddr));
 #pragma unroll
-  for (int k = 0; k < 4; ++k) d4[k] = make_float4(v[4 * k], v[4 * k + 1], v[4 * k + 2], v[4 * k + 3]);
+  for (int i = 0; i < 8; ++i) v[i] = __uint_as_float(r[i]);
 }
-__device__ __forceinline__ void store16u8(uint8_t* dst, const uint8_t (&a)[16]) {
-  uint32_t w[4];
-#pragma unroll
-  for (int k = 0; k < 4; ++k)
-    w[k] = a[4 * k] | (a[4 * k + 1] << 8) | (a[4 * k + 2] << 16) | ((uint32_t)a[4 * k + 3] << 24);
-  *reinterpret_cast<uint4*>(dst) = make_uint4(w[0], w[1], w[2], w[3]);
+__device__ __forceinline__ void tmem_ld2(uint32_t taddr, float* v) {
+  uint32_t r[2];
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x2.b32 {%0,%1}, [%2];\n" : "=r"(r[0]), "=r"(r[1]) : "r"(taddr));
+  v[0] = __uint_as_float(r[0]);
+  v[1] = __uint_as_float(r[1]);
 }
 
+// ---- pooling epilogue ------------------------------------------------------------------
 // max-fold of rotations [R0, R0+G) of this base into Yr[R0] (+ argmax, ties -> smallest
-// index); everything in place to keep the epilogue's register footprint at Y + 16.
+// index); in place to keep the register footprint at Y + staging.
 template <int R0, int G>
-__device__ __forceinline__ void fold_max(float (&Yr)[4][16], uint32_t (&arg)[4], int kk0) {
+__device__ __forceinline__ void fold_max(float (&Yr)[4][XH], uint32_t (&arg)[2], int kk0) {
 #pragma unroll
   for (int r = R0 + 1; r < R0 + G; ++r)
 #pragma unroll
-    for (int j = 0; j < 16; ++j)
+    for (int j = 0; j < XH; ++j)
       if (Yr[r][j] > Yr[R0][j]) {
         Yr[R0][j] = Yr[r][j];
         arg[j / 4] = (arg[j / 4] & ~(0xFFu << (8 * (j % 4)))) | ((uint32_t)(kk0 + r - R0) << (8 * (j % 4)));
       }
 }
-__device__ __forceinline__ void store_row(const TcParams& p, size_t off, float (&v)[16], const uint32_t (&arg)[4],
+__device__ __forceinline__ void store8(float* dst, const float (&v)[XH]) {
+  float4* d4 = reinterpret_cast<float4*>(dst);
+  d4[0] = make_float4(v[0], v[1], v[2], v[3]);
+  d4[1] = make_float4(v[4], v[5], v[6], v[7]);
+}
+__device__ __forceinline__ void store_row(const TcParams& p, size_t off, float (&v)[XH], const uint32_t (&arg)[2],
                                           float bz, bool fin) {
   if (fin) {
 #pragma unroll
-    for (int j = 0; j < 16; ++j) v[j] += bz;
+    for (int j = 0; j < XH; ++j) v[j] += bz;
   }
-  store16(p.y + off, v);
-  if (p.am) *reinterpret_cast<uint4*>(p.am + off) = make_uint4(arg[0], arg[1], arg[2], arg[3]);
+  store8(p.y + off, v);
+  if (p.am) *reinterpret_cast<uint2*>(p.am + off) = make_uint2(arg[0], arg[1]);
 }
 
-// pool + bias + store one output row (16 px) of base b; same semantics as ri_simt.cu.
+// pool + bias + store one output half-row (8 px) of base b; same semantics as ri_simt.cu.
 // Fold groups gf in {1, 2, 4} stay inside a base; gf % 4 == 0 spans bases through a
 // partial (value, argmax) kept in the output row itself (same thread, program order).
-__device__ __forceinline__ void finalize_row(const TcParams& p, float (&Yr)[4][16], int n, int co, int b,
-                                             int row) {
+__device__ __forceinline__ void finalize_row(const TcParams& p, float (&Yr)[4][XH], int n, int co, int b,
+                                             int row, int x0) {
   const size_t plane = (size_t)p.H * TW;
-  const size_t ybase = ((size_t)n * p.Cout + co) * p.RO * plane + (size_t)row * TW;
+  const size_t ybase = ((size_t)n * p.Cout + co) * p.RO * plane + (size_t)row * TW + x0;
   const float bz = p.bias ? p.bias[co] : 0.f;
   if (p.pool == RC_POOL_NONE) {
-    const uint32_t z[4] = {0, 0, 0, 0};
+    const uint32_t z[2] = {0, 0};
 #pragma unroll
     for (int r = 0; r < 4; ++r) store_row(p, ybase + (size_t)(b * 4 + r) * plane, Yr[r], z, bz, true);
     return;
@@ -121,39 +128,38 @@ __device__ __forceinline__ void finalize_row(const TcParams& p, float (&Yr)[4][1
   if (p.pool == RC_POOL_AVG) {
     if (b > 0) {
 #pragma unroll
-      for (int j = 0; j < 16; ++j) Yr[0][j] = p.y[ybase + j] + Yr[0][j];
+      for (int j = 0; j < XH; ++j) Yr[0][j] = p.y[ybase + j] + Yr[0][j];
     }
 #pragma unroll
     for (int r = 1; r < 4; ++r)
 #pragma unroll
-      for (int j = 0; j < 16; ++j) Yr[0][j] += Yr[r][j];
-    if (b == p.NB - 1) {
-      const float R = (float)(p.NB * 4);
+      for (int j = 0; j < XH; ++j) Yr[0][j] += Yr[r][j];
+    if (b == p.NB - 1) {  // R is a power of two here (tc_supported): x * (1/R) == x / R exactly
 #pragma unroll
-      for (int j = 0; j < 16; ++j) Yr[0][j] = Yr[0][j] / R + bz;
+      for (int j = 0; j < XH; ++j) Yr[0][j] = __fadd_rn(__fmul_rn(Yr[0][j], p.inv_r), bz);
     }
-    store16(p.y + ybase, Yr[0]);
+    store8(p.y + ybase, Yr[0]);
     return;
   }
   const int gf = p.gf;
-  uint32_t arg[4] = {0, 0, 0, 0};
+  uint32_t arg[2] = {0, 0};
   if (gf == 1) {
 #pragma unroll
     for (int r = 0; r < 4; ++r) store_row(p, ybase + (size_t)(b * 4 + r) * plane, Yr[r], arg, bz, true);
   } else if (gf == 2) {
     fold_max<0, 2>(Yr, arg, 0);
     store_row(p, ybase + (size_t)(b * 2) * plane, Yr[0], arg, bz, true);
-    arg[0] = arg[1] = arg[2] = arg[3] = 0;
+    arg[0] = arg[1] = 0;
     fold_max<2, 2>(Yr, arg, 0);
     store_row(p, ybase + (size_t)(b * 2 + 1) * plane, Yr[2], arg, bz, true);
   } else {  // gf % 4 == 0
     const int o0 = b * 4, slot = o0 / gf, kk0 = o0 - slot * gf;
     const size_t off = ybase + (size_t)slot * plane;
-    arg[0] = arg[1] = arg[2] = arg[3] = (uint32_t)kk0 * 0x01010101u;  // candidate r=0 is index kk0
+    arg[0] = arg[1] = (uint32_t)kk0 * 0x01010101u;  // candidate r=0 is index kk0
     fold_max<0, 4>(Yr, arg, kk0);
     if (kk0 > 0) {  // continue the slot begun in an earlier base
 #pragma unroll
-      for (int j = 0; j < 16; ++j) {
+      for (int j = 0; j < XH; ++j) {
         const float prev = p.y[off + j];
         const uint32_t pa = p.am ? p.am[off + j] : 0u;
         if (!(Yr[0][j] > prev)) {  // earlier (smaller) index wins ties
@@ -166,132 +172,131 @@ __device__ __forceinline__ void finalize_row(const TcParams& p, float (&Yr)[4][1
   }
 }
 
-// scatter one Z row of tap t into this warp half's 2 output rows (all indices
-// compile-time; t is dispatched once per call):
-//   row holds input row REL relative to the band start 4k;
-//   Y[l] is output row (BASE + l) relative to 4k.  Input row q feeds output q - di.
-template <int CONV, int REL, int BASE, int TT>
-__device__ __forceinline__ void scatter_row_t(float (&Y)[2][4][16], const float (&row)[16]) {
-  constexpr K3Tables TB = make_k3(CONV);
+// ---- scatter ------------------------------------------------------------------------
+// z[i] holds D-buffer row (2*rp + REL + i) = input row (4k - 1 + 2*rp + REL + i), as
+// loaded elements e = column (x0 - 1 + e).  Y[l] is output row (4k + 2*rp + l).
+// Y_r(p) += Z_t(p + (di, dj)):  input row q feeds output q - di, column x + dj feeds x.
+template <int CONV, int TT, int R, int REL>
+__device__ __forceinline__ void scatter_r(float (&Y)[2][4][XH], const float (&z)[2][ZW]) {
+  constexpr int DI = make_k3(CONV).di[R][TT];  // template constants: every index is static
+  constexpr int DJ = make_k3(CONV).dj[R][TT];
 #pragma unroll
-  for (int r = 0; r < 4; ++r) {
-    const int l = REL - TB.di[r][TT] - BASE;
+  for (int i = 0; i < 2; ++i) {
+    const int l = REL + i - 1 - DI;  // output local row fed by this input row
     if (l < 0 || l > 1) continue;
-    const int dj = TB.dj[r][TT];
 #pragma unroll
-    for (int x = 0; x < 16; ++x) {
-      const int src = x + dj;
-      if (src < 0 || src > 15) continue;
+    for (int xl = 0; xl < XH; ++xl) {
       if (l == 0)
-        Y[0][r][x] += row[src];
+        Y[0][R][xl] += z[i][xl + DJ + 1];
       else
-        Y[1][r][x] += row[src];
+        Y[1][R][xl] += z[i][xl + DJ + 1];
     }
   }
 }
-template <int CONV, int REL, int BASE>
-__device__ __forceinline__ void scatter_row(float (&Y)[2][4][16], const float (&row)[16], int t) {
+template <int CONV, int TT, int REL>
+__device__ __forceinline__ void scatter_tt(float (&Y)[2][4][XH], const float (&z)[2][ZW]) {
+  scatter_r<CONV, TT, 0, REL>(Y, z);
+  scatter_r<CONV, TT, 1, REL>(Y, z);
+  scatter_r<CONV, TT, 2, REL>(Y, z);
+  scatter_r<CONV, TT, 3, REL>(Y, z);
+}
+template <int CONV, int REL>
+__device__ __forceinline__ void scatter(float (&Y)[2][4][XH], const float (&z)[2][ZW], int t) {
   switch (t) {
-    case 0: scatter_row_t<CONV, REL, BASE, 0>(Y, row); break;
-    case 1: scatter_row_t<CONV, REL, BASE, 1>(Y, row); break;
-    case 2: scatter_row_t<CONV, REL, BASE, 2>(Y, row); break;
-    case 3: scatter_row_t<CONV, REL, BASE, 3>(Y, row); break;
-    case 4: scatter_row_t<CONV, REL, BASE, 4>(Y, row); break;
-    case 5: scatter_row_t<CONV, REL, BASE, 5>(Y, row); break;
-    case 6: scatter_row_t<CONV, REL, BASE, 6>(Y, row); break;
-    case 7: scatter_row_t<CONV, REL, BASE, 7>(Y, row); break;
-    default: scatter_row_t<CONV, REL, BASE, 8>(Y, row); break;
+    case 0: scatter_tt<CONV, 0, REL>(Y, z); break;
+    case 1: scatter_tt<CONV, 1, REL>(Y, z); break;
+    case 2: scatter_tt<CONV, 2, REL>(Y, z); break;
+    case 3: scatter_tt<CONV, 3, REL>(Y, z); break;
+    case 4: scatter_tt<CONV, 4, REL>(Y, z); break;
+    case 5: scatter_tt<CONV, 5, REL>(Y, z); break;
+    case 6: scatter_tt<CONV, 6, REL>(Y, z); break;
+    case 7: scatter_tt<CONV, 7, REL>(Y, z); break;
+    default: scatter_tt<CONV, 8, REL>(Y, z); break;
   }
 }
-template <int CONV, int REL, int BASE>
-__device__ __forceinline__ void load_scatter(float (&Y)[2][4][16], uint32_t taddr, int t) {
-  float row[16];
-  tmem_ld16(taddr, row);
+
+// load two D-buffer rows (10 columns each: x0-1 .. x0+8), zero the image-border column
+__device__ __forceinline__ void load_rows2(float (&z)[2][ZW], uint32_t taddr, int ch) {
+  tmem_ld8(taddr, z[0]);
+  tmem_ld2(taddr + 8, z[0] + 8);
+  tmem_ld8(taddr + TW, z[1]);
+  tmem_ld2(taddr + TW + 8, z[1] + 8);
   tmem_wait_ld();
-  scatter_row<CONV, REL, BASE>(Y, row, t);
-}
-__device__ __forceinline__ void copy_row(uint32_t src, uint32_t dst) {
-  float row[16];
-  tmem_ld16(src, row);
-  tmem_wait_ld();
-  tmem_st16(dst, row);
+#pragma unroll
+  for (int i = 0; i < 2; ++i) {
+    if (ch == 0)
+      z[i][0] = 0.f;  // column -1
+    else
+      z[i][ZW - 1] = 0.f;  // column 16
+  }
 }
 
-// Epilogue of one warp half over all work items.  H = 0: output rows 4k-1, 4k (needs
-// input rows -2..1: kept slot + new rows 0,1; also copies new rows 2,3 into the kept
-// slot for band k+1).  H = 1: output rows 4k+1, 4k+2 (needs new rows 0..3).
-// Z rows are pulled from TMEM one at a time (Y 128 + 16 staging registers).
-template <int CONV, int H>
+// Epilogue warp: lane quadrant q (co = q*32 + lane), sub-tile rp (output rows 2rp, 2rp+1 of
+// the band) x ch (columns 8ch .. 8ch+7).  Per tap two TMEM round trips of two rows each.
+template <int CONV>
 __device__ void epilogue(const TcParams& p, uint32_t tmem, uint64_t* d_full, uint64_t* d_empty) {
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int q = warp % 4;
+  const int sub = (warp - EPI_WARP0) / 4;
+  const int rp = sub >> 1, ch = sub & 1;
+  const int x0 = ch * XH;
   const int co_l = q * 32 + lane;
-  const uint32_t lane_off = (uint32_t)(q * 32) << 16;
-  constexpr int BASE = H == 0 ? -1 : 1;
-  uint32_t gd = 0;
-  float Y[2][4][16];
+  const uint32_t lane_base = tmem + ((uint32_t)(q * 32) << 16) + D0 + 2 * rp * TW + x0 - 1;
+  int db = 0;
+  uint32_t dph = 0;
+  float Y[2][4][XH];
   for (int item = blockIdx.x; item < p.items; item += gridDim.x) {
     const int ct = item / p.N, n = item % p.N;
     const int co = ct * 128 + co_l;
     for (int b = 0; b < p.NB; ++b)
-      for (int k = 0; k <= p.NBK; ++k) {  // k == NBK: drain band (no MMA, zero rows)
-        const bool have_new = k < p.NBK;
-        if (H == 1 && !have_new) continue;  // its rows 4*NBK+1.. are beyond H
+      for (int k = 0; k < p.NBK; ++k) {
 #pragma unroll
         for (int l = 0; l < 2; ++l)
 #pragma unroll
           for (int r = 0; r < 4; ++r)
 #pragma unroll
-            for (int x = 0; x < 16; ++x) Y[l][r][x] = 0.f;
+            for (int x = 0; x < XH; ++x) Y[l][r][x] = 0.f;
 #pragma unroll 1
         for (int t = 0; t < 9; ++t) {
-          const int db = gd & 1;
-          const uint32_t dcol = tmem + lane_off + db * BAND_PX;
-          const uint32_t kcol = tmem + lane_off + KEPT0 + t * 32;
-          if (H == 0) {
-            if (k > 0) {  // input rows -2, -1 from the kept slot (zero above the image)
-              load_scatter<CONV, -2, BASE>(Y, kcol, t);
-              load_scatter<CONV, -1, BASE>(Y, kcol + 16, t);
-            }
-            if (have_new) {
-              mbar_wait(&d_full[db], (gd >> 1) & 1);
-              tc_fence_after();
-              load_scatter<CONV, 0, BASE>(Y, dcol, t);
-              load_scatter<CONV, 1, BASE>(Y, dcol + 16, t);
-              copy_row(dcol + 32, kcol);  // rows 2, 3 -> kept slot (rows -2, -1 of band k+1)
-              copy_row(dcol + 48, kcol + 16);
-              tmem_wait_st();
-              tc_fence_before();
-              __syncwarp();
-              if (lane == 0) mbar_arrive(&d_empty[db]);
-              ++gd;
-            }
-          } else {
-            mbar_wait(&d_full[db], (gd >> 1) & 1);
-            tc_fence_after();
-            load_scatter<CONV, 0, BASE>(Y, dcol, t);
-            load_scatter<CONV, 1, BASE>(Y, dcol + 16, t);
-            load_scatter<CONV, 2, BASE>(Y, dcol + 32, t);
-            float row[16];
-            tmem_ld16(dcol + 48, row);
-            tmem_wait_ld();
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&d_empty[db]);
-            scatter_row<CONV, 3, BASE>(Y, row, t);
-            ++gd;
+          const uint32_t a = lane_base + db * BAND_PX;
+          float z[2][ZW];
+          mbar_wait(&d_full[db], dph);
+          tc_fence_after();
+          load_rows2(z, a, ch);
+          scatter<CONV, 0>(Y, z, t);
+          load_rows2(z, a + 2 * TW, ch);
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&d_empty[db]);  // D buffer free: MMA may refill it
+          if (++db == NDB) {
+            db = 0;
+            dph ^= 1;
           }
+          scatter<CONV, 2>(Y, z, t);
         }
         if (n < p.N && co < p.Cout) {
 #pragma unroll
           for (int l = 0; l < 2; ++l) {
-            const int row = BAND_ROWS * k + BASE + l;
-            if (row >= 0 && row < p.H) finalize_row(p, Y[l], n, co, b, row);
+            const int row = OUT_ROWS * k + 2 * rp + l;
+            if (row < p.H) finalize_row(p, Y[l], n, co, b, row, x0);
           }
         }
       }
   }
 }
+
+// smem ring position: stage index + phase parity, advanced without division
+struct Ring {
+  uint32_t s = 0, ph = 0;
+  bool used = false;
+  __device__ __forceinline__ void adv(int S) {
+    if (++s == (uint32_t)S) {
+      s = 0;
+      ph ^= 1;
+      used = true;
+    }
+  }
+};
 
 template <int CONV>
 __global__ void __launch_bounds__(THREADS, 1) ri_tc_kernel(const __grid_constant__ TcParams p) {
@@ -300,12 +305,13 @@ __global__ void __launch_bounds__(THREADS, 1) ri_tc_kernel(const __grid_constant
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const int parts = p.passes == 3 ? 2 : 1;
   const int xbuf_bytes = parts * p.NC * XTILE;
-  uint8_t* xs = smem;                      // 2 X band buffers
-  uint8_t* ws = smem + 2 * xbuf_bytes;     // W ring
-  __shared__ uint64_t w_full[8], w_empty[8], x_full[2], x_empty[2], d_full[2], d_empty[2];
+  const int XB = p.x_bufs;               // 1 or 2 X band buffers
+  uint8_t* xs = smem;
+  uint8_t* ws = smem + XB * xbuf_bytes;  // W ring
+  __shared__ uint64_t w_full[8], w_empty[8], x_full[2], x_empty[2], d_full[NDB], d_empty[NDB];
   __shared__ uint32_t tmem_base_sh;
 
-  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int warp = threadIdx.x / 32;
   const int S = p.w_stages;
   if (threadIdx.x == 0) {
     for (int s = 0; s < S; ++s) {
@@ -315,6 +321,8 @@ __global__ void __launch_bounds__(THREADS, 1) ri_tc_kernel(const __grid_constant
     for (int i = 0; i < 2; ++i) {
       mbar_init(&x_full[i], 1);
       mbar_init(&x_empty[i], 1);
+    }
+    for (int i = 0; i < NDB; ++i) {
       mbar_init(&d_full[i], 1);
       mbar_init(&d_empty[i], NUM_EPI);
     }
@@ -326,119 +334,128 @@ __global__ void __launch_bounds__(THREADS, 1) ri_tc_kernel(const __grid_constant
   tc_fence_after();
   const uint32_t tmem = tmem_base_sh;
 
+  // W stage = spc consecutive ci-chunks of one tap (hi, or hi+lo interleaved), ONE bulk
+  // copy of >= 32 KB: the TMA engine's per-copy cost makes small copies the bottleneck
+  // (profiles/r01/l2_microbench.jsonl).
+  const int stage_bytes = p.spc * parts * WTILE;
+  const int stages_per_tap = p.NC / p.spc;
+  if (warp < EPI_WARP0) asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(REGS_PRODUCER));
   if (warp == 0) {
-    // ------------------------------------------------------------ producer
-    if (lane == 0) {
-      uint32_t gw = 0, xc = 0;
-      for (int item = blockIdx.x; item < p.items; item += gridDim.x) {
-        const int ct = item / p.N, n = item % p.N;
-        for (int b = 0; b < p.NB; ++b)
-          for (int k = 0; k < p.NBK; ++k) {
-            const int xb = xc & 1;
-            if (xc >= 2) mbar_wait(&x_empty[xb], ((xc >> 1) & 1) ^ 1);
+    // ------------------------------------------------------------ producer (whole warp
+    // walks the schedule; one elected lane issues the bulk copies)
+    Ring wr;
+    uint32_t xc = 0;
+    for (int item = blockIdx.x; item < p.items; item += gridDim.x) {
+      const int ct = item / p.N, n = item % p.N;
+      for (int b = 0; b < p.NB; ++b)
+        for (int k = 0; k < p.NBK; ++k) {
+          const int xb = XB == 2 ? (xc & 1) : 0;
+          const uint32_t xuse = XB == 2 ? (xc >> 1) : xc;  // uses of this buffer so far
+          if (xuse > 0) mbar_wait(&x_empty[xb], (xuse - 1) & 1);
+          if (elect_one()) {
             mbar_arrive_expect_tx(&x_full[xb], xbuf_bytes);
-            for (int part = 0; part < parts; ++part)
-              for (int c = 0; c < p.NC; ++c) {
-                const size_t tile = ((size_t)n * p.NBK + k) * p.NC + c;
-                bulk_g2s(xs + xb * xbuf_bytes + (part * p.NC + c) * XTILE,
-                         (part ? p.xl : p.xh) + tile * XTILE, XTILE, &x_full[xb]);
-              }
-            ++xc;
-            for (int t = 0; t < 9; ++t)
-              for (int c = 0; c < p.NC; ++c)
-                for (int part = 0; part < parts; ++part) {
-                  const int s = gw % S;
-                  if (gw >= (uint32_t)S) mbar_wait(&w_empty[s], ((gw / S) & 1) ^ 1);
-                  mbar_arrive_expect_tx(&w_full[s], WTILE);
-                  const size_t tile = (((size_t)b * p.NCT + ct) * 9 + t) * p.NC + c;
-                  bulk_g2s(ws + s * WTILE, (part ? p.wl : p.wh) + tile * WTILE, WTILE, &w_full[s]);
-                  ++gw;
-                }
+            const size_t tile = ((size_t)n * p.NBK + k) * p.NC;
+            bulk_g2s(xs + xb * xbuf_bytes, p.xh + tile * XTILE, p.NC * XTILE, &x_full[xb]);
+            if (parts == 2)
+              bulk_g2s(xs + xb * xbuf_bytes + p.NC * XTILE, p.xl + tile * XTILE, p.NC * XTILE, &x_full[xb]);
           }
-      }
+          __syncwarp();
+          ++xc;
+          const uint8_t* wsrc = p.w + (((size_t)b * p.NCT + ct) * 9) * p.NC * parts * WTILE;
+          for (int st = 0; st < 9 * stages_per_tap; ++st) {
+            if (wr.used) mbar_wait(&w_empty[wr.s], wr.ph ^ 1);
+            if (elect_one()) {
+              mbar_arrive_expect_tx(&w_full[wr.s], stage_bytes);
+              bulk_g2s(ws + wr.s * stage_bytes, wsrc + (size_t)st * stage_bytes, stage_bytes, &w_full[wr.s]);
+            }
+            __syncwarp();
+            wr.adv(S);
+          }
+        }
     }
   } else if (warp == 1) {
-    // ------------------------------------------------------------ MMA issuer
-    if (lane == 0) {
-      const uint32_t idesc = idesc_bf16_f32(128, BAND_PX);
-      uint32_t gw = 0, xc = 0, gd = 0;
-      for (int item = blockIdx.x; item < p.items; item += gridDim.x) {
-        for (int b = 0; b < p.NB; ++b)
-          for (int k = 0; k < p.NBK; ++k) {
-            const int xb = xc & 1;
-            mbar_wait(&x_full[xb], (xc >> 1) & 1);
+    // ------------------------------------------------------------ MMA issuer (whole warp
+    // waits; one elected lane issues tcgen05.mma + commits)
+    const uint32_t idesc = idesc_bf16_f32(128, BAND_PX);
+    Ring wr;
+    uint32_t xc = 0, gd = 0;
+    int db = 0;
+    uint32_t dph = 0;
+    for (int item = blockIdx.x; item < p.items; item += gridDim.x) {
+      for (int b = 0; b < p.NB; ++b)
+        for (int k = 0; k < p.NBK; ++k) {
+          const int xb = XB == 2 ? (xc & 1) : 0;
+          const uint32_t xuse = XB == 2 ? (xc >> 1) : xc;
+          mbar_wait(&x_full[xb], xuse & 1);
+          tc_fence_after();
+          const uint32_t xaddr = smem_u32(xs + xb * xbuf_bytes);
+          for (int t = 0; t < 9; ++t) {
+            if (gd >= NDB) mbar_wait(&d_empty[db], dph ^ 1);
             tc_fence_after();
-            const uint32_t xaddr = smem_u32(xs + xb * xbuf_bytes);
-            for (int t = 0; t < 9; ++t) {
-              const int db = gd & 1;
-              if (gd >= 2) mbar_wait(&d_empty[db], ((gd >> 1) & 1) ^ 1);
+            const uint32_t d = tmem + D0 + db * BAND_PX;
+            for (int sp = 0; sp < stages_per_tap; ++sp) {
+              mbar_wait(&w_full[wr.s], wr.ph);
               tc_fence_after();
-              const uint32_t d = tmem + db * BAND_PX;
-              for (int c = 0; c < p.NC; ++c) {
-                const uint64_t bh = desc_k_sw128(xaddr + c * XTILE);
-                if (parts == 1) {
-                  const int s = gw % S;
-                  mbar_wait(&w_full[s], (gw / S) & 1);
-                  tc_fence_after();
-                  const uint64_t a = desc_k_sw128(smem_u32(ws + s * WTILE));
-#pragma unroll
-                  for (int kk = 0; kk < 4; ++kk) mma_bf16_ss(d, a + 2 * kk, bh + 2 * kk, idesc, (c | kk) != 0);
-                  mma_commit(&w_empty[s]);
-                  ++gw;
-                } else {
-                  const uint64_t bl = desc_k_sw128(xaddr + (p.NC + c) * XTILE);
-                  const int sh = gw % S, sl = (gw + 1) % S;
-                  mbar_wait(&w_full[sh], (gw / S) & 1);
-                  mbar_wait(&w_full[sl], ((gw + 1) / S) & 1);
-                  tc_fence_after();
-                  const uint64_t ah = desc_k_sw128(smem_u32(ws + sh * WTILE));
-                  const uint64_t al = desc_k_sw128(smem_u32(ws + sl * WTILE));
+              if (elect_one()) {
+                const uint32_t wbase = smem_u32(ws + wr.s * stage_bytes);
+                for (int cl = 0; cl < p.spc; ++cl) {
+                  const int c = sp * p.spc + cl;
+                  const uint64_t bh = desc_k_sw128(xaddr + c * XTILE);
+                  const uint64_t ah = desc_k_sw128(wbase + cl * parts * WTILE);
 #pragma unroll
                   for (int kk = 0; kk < 4; ++kk) mma_bf16_ss(d, ah + 2 * kk, bh + 2 * kk, idesc, (c | kk) != 0);
+                  if (parts == 2) {
+                    const uint64_t bl = desc_k_sw128(xaddr + (p.NC + c) * XTILE);
+                    const uint64_t al = desc_k_sw128(wbase + (cl * parts + 1) * WTILE);
 #pragma unroll
-                  for (int kk = 0; kk < 4; ++kk) mma_bf16_ss(d, ah + 2 * kk, bl + 2 * kk, idesc, 1);
+                    for (int kk = 0; kk < 4; ++kk) mma_bf16_ss(d, ah + 2 * kk, bl + 2 * kk, idesc, 1);
 #pragma unroll
-                  for (int kk = 0; kk < 4; ++kk) mma_bf16_ss(d, al + 2 * kk, bh + 2 * kk, idesc, 1);
-                  mma_commit(&w_empty[sh]);
-                  mma_commit(&w_empty[sl]);
-                  gw += 2;
+                    for (int kk = 0; kk < 4; ++kk) mma_bf16_ss(d, al + 2 * kk, bh + 2 * kk, idesc, 1);
+                  }
                 }
+                mma_commit(&w_empty[wr.s]);
+                if (sp == stages_per_tap - 1) mma_commit(&d_full[db]);
               }
-              mma_commit(&d_full[db]);
-              ++gd;
+              __syncwarp();
+              wr.adv(S);
             }
-            mma_commit(&x_empty[xb]);
-            ++xc;
+            ++gd;
+            if (++db == NDB) {
+              db = 0;
+              dph ^= 1;
+            }
           }
-      }
+          if (elect_one()) mma_commit(&x_empty[xb]);
+          __syncwarp();
+          ++xc;
+        }
     }
-  } else {
+  } else if (warp >= EPI_WARP0) {
     // ------------------------------------------------------------ epilogue
-    if ((warp - 2) / 4 == 0)
-      epilogue<CONV, 0>(p, tmem, d_full, d_empty);
-    else
-      epilogue<CONV, 1>(p, tmem, d_full, d_empty);
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(REGS_EPILOGUE));
+    epilogue<CONV>(p, tmem, d_full, d_empty);
   }
   tc_fence_before();
   __syncthreads();
   if (warp == 1) tmem_dealloc<512>(tmem);
 }
 
-// ---- packing kernels ----------------------------------------------------------------
+// ---- packing kernels ------------------------------------------------------------------
 __device__ __forceinline__ void split_bf16(float v, __nv_bfloat16& hi, __nv_bfloat16& lo) {
   hi = __float2bfloat16_rn(v);
   lo = __float2bfloat16_rn(v - __bfloat162float(hi));
 }
 
-// X fp32 NCHW (W = 16) -> SW128 bf16 tiles [n][band][chunk][64 px][64 ci] (hi, lo planes)
+// X fp32 NCHW (W = 16) -> SW128 bf16 tiles [n][band k][chunk][96 px][64 ci] (hi, lo planes);
+// band k holds input rows 4k-1 .. 4k+4, rows outside the image are zero (the padding).
 __global__ void x_pack_kernel(const float* __restrict__ x, uint8_t* __restrict__ xh,
                               uint8_t* __restrict__ xl, int Cin, int H, int NBK, int NC) {
   __shared__ float tile[KC][BAND_PX + 1];
   const int c = blockIdx.x, k = blockIdx.y, n = blockIdx.z;
   for (int i = threadIdx.x; i < KC * BAND_PX; i += blockDim.x) {
     const int cl = i / BAND_PX, px = i % BAND_PX;
-    const int ci = c * KC + cl, row = k * BAND_ROWS + px / TW, col = px % TW;
-    tile[cl][px] = (ci < Cin && row < H) ? x[(((size_t)n * Cin + ci) * H + row) * TW + col] : 0.f;
+    const int ci = c * KC + cl, row = k * OUT_ROWS - 1 + px / TW, col = px % TW;
+    tile[cl][px] = (ci < Cin && row >= 0 && row < H) ? x[(((size_t)n * Cin + ci) * H + row) * TW + col] : 0.f;
   }
   __syncthreads();
   const size_t tidx = ((size_t)n * NBK + k) * NC + c;
@@ -455,9 +472,11 @@ __global__ void x_pack_kernel(const float* __restrict__ x, uint8_t* __restrict__
   }
 }
 
-// base kernels fp32 [B][Cout][Cin][9] -> SW128 bf16 tiles [b][ct][t][chunk][128 co][64 ci]
-__global__ void w_pack_kernel(const float* __restrict__ bases, uint8_t* __restrict__ wh,
-                              uint8_t* __restrict__ wl, int NB, int Cout, int Cin, int NCT, int NC) {
+// base kernels fp32 [B][Cout][Cin][9] -> SW128 bf16 tiles [b][ct][t][chunk][part][128 co][64 ci]
+// (part 0 = hi, 1 = lo) for bf16x3, plus a hi-only copy [b][ct][t][chunk] for bf16 so that
+// every W stage is one contiguous bulk copy in both precisions.
+__global__ void w_pack_kernel(const float* __restrict__ bases, uint8_t* __restrict__ w,
+                              uint8_t* __restrict__ whi, int NB, int Cout, int Cin, int NCT, int NC) {
   const long long total = (long long)NB * NCT * 9 * NC * 128 * (KC / 8);
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
        i += (long long)gridDim.x * blockDim.x) {
@@ -476,9 +495,11 @@ __global__ void w_pack_kernel(const float* __restrict__ bases, uint8_t* __restri
       const float v = (co < Cout && ci < Cin) ? bases[(((size_t)b * Cout + co) * Cin + ci) * 9 + t] : 0.f;
       split_bf16(v, h8[j], l8[j]);
     }
-    const size_t off = (size_t)tile * WTILE + sw128_offset(col, g * 8);
-    *reinterpret_cast<uint4*>(wh + off) = *reinterpret_cast<const uint4*>(h8);
-    *reinterpret_cast<uint4*>(wl + off) = *reinterpret_cast<const uint4*>(l8);
+    const size_t off = (size_t)tile * 2 * WTILE + sw128_offset(col, g * 8);  // [tile][part]
+    *reinterpret_cast<uint4*>(w + off) = *reinterpret_cast<const uint4*>(h8);
+    *reinterpret_cast<uint4*>(w + off + WTILE) = *reinterpret_cast<const uint4*>(l8);
+    *reinterpret_cast<uint4*>(whi + (size_t)tile * WTILE + sw128_offset(col, g * 8)) =
+        *reinterpret_cast<const uint4*>(h8);
   }
 }
 
@@ -488,7 +509,7 @@ struct TcGeom {
 };
 TcGeom geom(const rc_desc& d) {
   TcGeom g;
-  g.NBK = (d.h + BAND_ROWS - 1) / BAND_ROWS;
+  g.NBK = (d.h + OUT_ROWS - 1) / OUT_ROWS;
   g.NC = (d.c_in + KC - 1) / KC;
   g.NCT = (d.c_out + 127) / 128;
   g.x_plane = (size_t)d.n * g.NBK * g.NC * XTILE;
@@ -496,17 +517,51 @@ TcGeom geom(const rc_desc& d) {
   return g;
 }
 
+struct SmemPlan {
+  int spc, stages, x_bufs;
+  size_t bytes;
+};
+// largest W stage (chunks per stage dividing NC) that leaves >= 2 stages; two X band
+// buffers when they fit next to two W stages of >= 32 KB, else one
+SmemPlan smem_plan(const TcGeom& g, int parts) {
+  SmemPlan sp{0, 0, 0, 0};
+  const size_t cap = 232448 - 1024 - 1024;  // dynamic smem minus alignment slack / statics
+  const size_t xbuf = (size_t)parts * g.NC * XTILE;
+  const size_t chunk = (size_t)parts * WTILE;
+  for (int xb = 2; xb >= 1 && sp.spc == 0; --xb) {
+    if (xb * xbuf >= cap) continue;
+    const size_t budget = cap - xb * xbuf;
+    for (int c = g.NC; c >= 1; --c) {
+      if (g.NC % c) continue;
+      const size_t sb = c * chunk;
+      if (2 * sb <= budget && (sb >= 32768 || c == g.NC || xb == 1)) {
+        sp.spc = c;
+        sp.stages = (int)(budget / sb) > 8 ? 8 : (int)(budget / sb);
+        sp.x_bufs = xb;
+        sp.bytes = xb * xbuf + sp.stages * sb + 1024;
+        break;
+      }
+    }
+  }
+  return sp;
+}
+
 }  // namespace
 
 bool tc_supported(const rc_desc& d) {
   const int gf = pool_fold(d);
-  const bool fold_ok = d.pool == RC_POOL_NONE || d.pool == RC_POOL_AVG || gf == 1 || gf == 2 || gf % 4 == 0;
-  return d.k == 3 && d.w == TW && d.group != RC_GROUP_SINGLE && d.c_in <= 512 && fold_ok &&
-         (d.precision == RC_PREC_BF16 || d.precision == RC_PREC_BF16X3 || d.precision == RC_PREC_AUTO);
+  const int R = d.orientations;
+  const bool fold_ok = d.pool == RC_POOL_NONE || (d.pool == RC_POOL_AVG && (R & (R - 1)) == 0) || gf == 1 ||
+                       gf == 2 || gf % 4 == 0;
+  if (!(d.k == 3 && d.w == TW && d.group != RC_GROUP_SINGLE && fold_ok &&
+        (d.precision == RC_PREC_BF16 || d.precision == RC_PREC_BF16X3 || d.precision == RC_PREC_AUTO)))
+    return false;
+  const int parts = d.precision == RC_PREC_BF16 ? 1 : 2;
+  return smem_plan(geom(d), parts).spc > 0;
 }
 size_t tc_bank_bytes(const rc_desc& d) {
   if (!(d.k == 3 && d.group != RC_GROUP_SINGLE)) return 0;
-  return 2 * geom(d).w_plane;
+  return 3 * geom(d).w_plane;  // interleaved hi/lo + hi-only
 }
 size_t tc_workspace_bytes(const rc_desc& d) {
   if (!tc_supported(d)) return 0;
@@ -518,7 +573,7 @@ int launch_tc_wpack(const rc_desc& d, const float* bases, uint8_t* tc_section, c
   const long long total = (long long)num_bases(d) * g.NCT * 9 * g.NC * 128 * (KC / 8);
   long long grid = (total + 255) / 256;
   if (grid > 148 * 16) grid = 148 * 16;
-  w_pack_kernel<<<(int)grid, 256, 0, s>>>(bases, tc_section, tc_section + g.w_plane, num_bases(d), d.c_out,
+  w_pack_kernel<<<(int)grid, 256, 0, s>>>(bases, tc_section, tc_section + 2 * g.w_plane, num_bases(d), d.c_out,
                                          d.c_in, g.NCT, g.NC);
   RC_CUDA(cudaGetLastError());
   return RC_OK;
@@ -533,17 +588,18 @@ int launch_tc(const rc_desc& d, const float* x, const void* bank, const float* b
   if (ws_bytes < tc_workspace_bytes(d) || ws == nullptr)
     return fail(RC_ERR_WORKSPACE, "ri_conv: workspace too small for the tensor-core path");
   const int passes = d.precision == RC_PREC_BF16 ? 1 : 3;
+  const int parts = passes == 3 ? 2 : 1;
   uint8_t* xh = static_cast<uint8_t*>(ws);
   uint8_t* xl = passes == 3 ? xh + g.x_plane : nullptr;
   x_pack_kernel<<<dim3(g.NC, g.NBK, d.n), 256, 0, s>>>(x, xh, xl, d.c_in, d.h, g.NBK, g.NC);
   RC_CUDA(cudaGetLastError());
   const BankLayout L = bank_layout(d);
   const uint8_t* tcb = static_cast<const uint8_t*>(bank) + L.tc_off;
+  const SmemPlan plan = smem_plan(g, parts);
   TcParams p;
   p.xh = xh;
   p.xl = xl;
-  p.wh = tcb;
-  p.wl = tcb + g.w_plane;
+  p.w = passes == 3 ? tcb : tcb + 2 * g.w_plane;
   p.bias = bias;
   p.y = y;
   p.am = (d.pool == RC_POOL_MAX || d.pool == RC_POOL_SUBGROUP) ? am : nullptr;
@@ -558,21 +614,18 @@ int launch_tc(const rc_desc& d, const float* x, const void* bank, const float* b
   p.gf = pool_fold(d);
   p.RO = out_orientations(d);
   p.passes = passes;
-  const int parts = passes == 3 ? 2 : 1;
-  const size_t xbytes = 2 * (size_t)parts * g.NC * XTILE;
-  int stages = (int)((220 * 1024 - xbytes) / WTILE);
-  if (stages > 8) stages = 8;
-  if (stages < 2 * parts) return fail(RC_ERR_UNSUPPORTED, "ri_conv: Cin too large for the tensor-core path");
-  p.w_stages = stages;
+  p.inv_r = 1.0f / (float)d.orientations;
+  p.w_stages = plan.stages;
+  p.spc = plan.spc;
+  p.x_bufs = plan.x_bufs;
   p.items = g.NCT * d.n;
-  const size_t smem = xbytes + (size_t)stages * WTILE + 1024;
   int dev, sms;
   RC_CUDA(cudaGetDevice(&dev));
   RC_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
   const int grid = p.items < sms ? p.items : sms;
   auto fn = d.convention == RC_CONV_RAW ? ri_tc_kernel<1> : ri_tc_kernel<0>;
-  RC_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  fn<<<grid, THREADS, smem, s>>>(p);
+  RC_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)plan.bytes));
+  fn<<<grid, THREADS, plan.bytes, s>>>(p);
   RC_CUDA(cudaGetLastError());
   return RC_OK;
 }

@@ -92,7 +92,7 @@ __global__ void __launch_bounds__(64, 1)
 
 template <int TILE, int STAGES>
 void run(const uint8_t* src, size_t region, long long* cyc, int sms, int per_sm, int mode) {
-  const int ntiles = 3000;
+  const int ntiles = 48000000 / TILE * 4;
   auto fn = stream_kernel<TILE, STAGES>;
   cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, STAGES * TILE);
   const int grid = sms * per_sm;
@@ -137,11 +137,9 @@ int main() {
   int sms;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
   run<16384, 4>(src, region, cyc, sms, 1, 0);
-  run<16384, 8>(src, region, cyc, sms, 1, 0);
-  run<16384, 4>(src, region, cyc, sms, 2, 0);
-  run<32768, 6>(src, region, cyc, sms, 1, 0);
-  run<16384, 8>(src, region, cyc, sms, 1, 1);
-  run<16384, 8>(src, region, cyc, sms, 1, 2);
-  run<16384, 8>(src, region, cyc, sms, 1, 3);
+  run<32768, 4>(src, region, cyc, sms, 1, 0);
+  run<65536, 3>(src, region, cyc, sms, 1, 0);
+  run<98304, 2>(src, region, cyc, sms, 1, 0);
+  run<65536, 2>(src, region, cyc, sms, 1, 1);
   return 0;
 }
