@@ -20,12 +20,14 @@
 //                           NDB TMEM buffers per (base, band, tap) and commits to mbarriers.
 //   warps 2, 3  idle (complete the producer warpgroup for setmaxnreg).
 //   warps 4-19  epilogue  : TMEM lane = output channel co.  The 4 warps of a lane quadrant
-//                           split the band into (2 output rows) x (8 columns); each thread
-//                           holds Y[2 rows][4 rotations][8 px] = 64 fp32 registers, reads
-//                           the 4 input rows it needs (10 columns incl. halo) straight from
-//                           TMEM, scatters with compile-time offsets, then pools + stores.
+//                           own the band's 4 output rows (one each); a thread holds
+//                           Y[4 rotations][16 px] = 64 fp32 registers, pulls the 3 input rows
+//                           it needs from TMEM (one 16-column load each), scatters with
+//                           compile-time offsets (taps unrolled), then pools + stores.
 // Pooling / argmax / bias epilogue identical to the SIMT kernel; 128-bit stores.
 #include <cuda_bf16.h>
+
+#include <cstdlib>
 
 #include "k3_tables.cuh"
 #include "rc_internal.cuh"
@@ -46,13 +48,12 @@ constexpr int WTILE = 128 * KC * 2;      // 16 KB
 constexpr int NUM_EPI = 16;              // epilogue warps (4 warpgroups)
 constexpr int EPI_WARP0 = 4;             // warps 0-3: producer warpgroup (TMA, MMA, 2 idle)
 constexpr int THREADS = 32 * (EPI_WARP0 + NUM_EPI);
-constexpr int REGS_PRODUCER = 40;        // setmaxnreg budgets: 20 warps x 96 at launch
-constexpr int REGS_EPILOGUE = 104;
+constexpr int REGS_PRODUCER = 32;        // setmaxnreg budgets: 20 warps x 96 at launch
+constexpr int REGS_EPILOGUE = 112;
 constexpr int NDB = 4;                   // TMEM accumulator buffers (MMA <-> epilogue)
 constexpr uint32_t D0 = 16;              // D buffers from column 16: the 1-column-left halo
                                          // load of a row stays inside the allocation
-constexpr int XH = 8;                    // output columns per epilogue thread
-constexpr int ZW = XH + 2;               // loaded columns incl. the halo on both sides
+constexpr int XH = TW;                   // output columns per epilogue thread (a full row)
 // TMEM columns: 16 + 4 * 96 = 400 <= 512
 
 struct TcParams {
@@ -64,6 +65,7 @@ struct TcParams {
   uint8_t* am;
   int N, H, Cout, NB, NBK, NC, NCT, pool, gf, RO, passes, w_stages, spc, x_bufs, items;
   float inv_r;  // 1/R for average pooling (R a power of two)
+  int ablate;   // profiling only: 1 = skip epilogue math, 2 = skip MMAs, 3 = skip MMAs + W loads
 };
 
 // ---- TMEM -> registers ----------------------------------------------------------------
@@ -86,7 +88,7 @@ __device__ __forceinline__ void tmem_ld2(uint32_t taddr, float* v) {
 // max-fold of rotations [R0, R0+G) of this base into Yr[R0] (+ argmax, ties -> smallest
 // index); in place to keep the register footprint at Y + staging.
 template <int R0, int G>
-__device__ __forceinline__ void fold_max(float (&Yr)[4][XH], uint32_t (&arg)[2], int kk0) {
+__device__ __forceinline__ void fold_max(float (&Yr)[4][XH], uint32_t (&arg)[XH / 4], int kk0) {
 #pragma unroll
   for (int r = R0 + 1; r < R0 + G; ++r)
 #pragma unroll
@@ -98,20 +100,20 @@ __device__ __forceinline__ void fold_max(float (&Yr)[4][XH], uint32_t (&arg)[2],
 }
 __device__ __forceinline__ void store8(float* dst, const float (&v)[XH]) {
   float4* d4 = reinterpret_cast<float4*>(dst);
-  d4[0] = make_float4(v[0], v[1], v[2], v[3]);
-  d4[1] = make_float4(v[4], v[5], v[6], v[7]);
+#pragma unroll
+  for (int k = 0; k < XH / 4; ++k) d4[k] = make_float4(v[4 * k], v[4 * k + 1], v[4 * k + 2], v[4 * k + 3]);
 }
-__device__ __forceinline__ void store_row(const TcParams& p, size_t off, float (&v)[XH], const uint32_t (&arg)[2],
-                                          float bz, bool fin) {
+__device__ __forceinline__ void store_row(const TcParams& p, size_t off, float (&v)[XH],
+                                          const uint32_t (&arg)[XH / 4], float bz, bool fin) {
   if (fin) {
 #pragma unroll
     for (int j = 0; j < XH; ++j) v[j] += bz;
   }
   store8(p.y + off, v);
-  if (p.am) *reinterpret_cast<uint2*>(p.am + off) = make_uint2(arg[0], arg[1]);
+  if (p.am) *reinterpret_cast<uint4*>(p.am + off) = make_uint4(arg[0], arg[1], arg[2], arg[3]);
 }
 
-// pool + bias + store one output half-row (8 px) of base b; same semantics as ri_simt.cu.
+// pool + bias + store one output row (16 px) of base b; same semantics as ri_simt.cu.
 // Fold groups gf in {1, 2, 4} stay inside a base; gf % 4 == 0 spans bases through a
 // partial (value, argmax) kept in the output row itself (same thread, program order).
 __device__ __forceinline__ void finalize_row(const TcParams& p, float (&Yr)[4][XH], int n, int co, int b,
@@ -120,7 +122,7 @@ __device__ __forceinline__ void finalize_row(const TcParams& p, float (&Yr)[4][X
   const size_t ybase = ((size_t)n * p.Cout + co) * p.RO * plane + (size_t)row * TW + x0;
   const float bz = p.bias ? p.bias[co] : 0.f;
   if (p.pool == RC_POOL_NONE) {
-    const uint32_t z[2] = {0, 0};
+    const uint32_t z[XH / 4] = {0, 0, 0, 0};
 #pragma unroll
     for (int r = 0; r < 4; ++r) store_row(p, ybase + (size_t)(b * 4 + r) * plane, Yr[r], z, bz, true);
     return;
@@ -142,20 +144,20 @@ __device__ __forceinline__ void finalize_row(const TcParams& p, float (&Yr)[4][X
     return;
   }
   const int gf = p.gf;
-  uint32_t arg[2] = {0, 0};
+  uint32_t arg[XH / 4] = {0, 0, 0, 0};
   if (gf == 1) {
 #pragma unroll
     for (int r = 0; r < 4; ++r) store_row(p, ybase + (size_t)(b * 4 + r) * plane, Yr[r], arg, bz, true);
   } else if (gf == 2) {
     fold_max<0, 2>(Yr, arg, 0);
     store_row(p, ybase + (size_t)(b * 2) * plane, Yr[0], arg, bz, true);
-    arg[0] = arg[1] = 0;
+    arg[0] = arg[1] = arg[2] = arg[3] = 0;
     fold_max<2, 2>(Yr, arg, 0);
     store_row(p, ybase + (size_t)(b * 2 + 1) * plane, Yr[2], arg, bz, true);
   } else {  // gf % 4 == 0
     const int o0 = b * 4, slot = o0 / gf, kk0 = o0 - slot * gf;
     const size_t off = ybase + (size_t)slot * plane;
-    arg[0] = arg[1] = (uint32_t)kk0 * 0x01010101u;  // candidate r=0 is index kk0
+    arg[0] = arg[1] = arg[2] = arg[3] = (uint32_t)kk0 * 0x01010101u;  // candidate r=0 is index kk0
     fold_max<0, 4>(Yr, arg, kk0);
     if (kk0 > 0) {  // continue the slot begun in an earlier base
 #pragma unroll
@@ -173,114 +175,86 @@ __device__ __forceinline__ void finalize_row(const TcParams& p, float (&Yr)[4][X
 }
 
 // ---- scatter ------------------------------------------------------------------------
-// z[i] holds D-buffer row (2*rp + REL + i) = input row (4k - 1 + 2*rp + REL + i), as
-// loaded elements e = column (x0 - 1 + e).  Y[l] is output row (4k + 2*rp + l).
-// Y_r(p) += Z_t(p + (di, dj)):  input row q feeds output q - di, column x + dj feeds x.
-template <int CONV, int TT, int R, int REL>
-__device__ __forceinline__ void scatter_r(float (&Y)[2][4][XH], const float (&z)[2][ZW]) {
-  constexpr int DI = make_k3(CONV).di[R][TT];  // template constants: every index is static
-  constexpr int DJ = make_k3(CONV).dj[R][TT];
+// Output row o = 4k + s of warp sub-tile s reads D-buffer rows s .. s+2 (input rows o-1 ..
+// o+1).  Y_r(p) += Z_t(p + (di, dj)): for tap T and rotation r the single contributing row
+// is I = 1 + di; columns x + dj outside [0, 16) are the zero padding and are skipped.
+template <int CONV, int T, int I>
+__device__ __forceinline__ void scatter_row(float (&Y)[4][XH], const float (&z)[16]) {
 #pragma unroll
-  for (int i = 0; i < 2; ++i) {
-    const int l = REL + i - 1 - DI;  // output local row fed by this input row
-    if (l < 0 || l > 1) continue;
+  for (int r = 0; r < 4; ++r) {
+    const int di = make_k3(CONV).di[r][T];
+    const int dj = make_k3(CONV).dj[r][T];
+    if (1 + di != I) continue;
 #pragma unroll
-    for (int xl = 0; xl < XH; ++xl) {
-      if (l == 0)
-        Y[0][R][xl] += z[i][xl + DJ + 1];
-      else
-        Y[1][R][xl] += z[i][xl + DJ + 1];
+    for (int x = 0; x < XH; ++x) {
+      const int src = x + dj;
+      if (src < 0 || src >= TW) continue;
+      Y[r][x] += z[src];
     }
   }
 }
-template <int CONV, int TT, int REL>
-__device__ __forceinline__ void scatter_tt(float (&Y)[2][4][XH], const float (&z)[2][ZW]) {
-  scatter_r<CONV, TT, 0, REL>(Y, z);
-  scatter_r<CONV, TT, 1, REL>(Y, z);
-  scatter_r<CONV, TT, 2, REL>(Y, z);
-  scatter_r<CONV, TT, 3, REL>(Y, z);
-}
-template <int CONV, int REL>
-__device__ __forceinline__ void scatter(float (&Y)[2][4][XH], const float (&z)[2][ZW], int t) {
-  switch (t) {
-    case 0: scatter_tt<CONV, 0, REL>(Y, z); break;
-    case 1: scatter_tt<CONV, 1, REL>(Y, z); break;
-    case 2: scatter_tt<CONV, 2, REL>(Y, z); break;
-    case 3: scatter_tt<CONV, 3, REL>(Y, z); break;
-    case 4: scatter_tt<CONV, 4, REL>(Y, z); break;
-    case 5: scatter_tt<CONV, 5, REL>(Y, z); break;
-    case 6: scatter_tt<CONV, 6, REL>(Y, z); break;
-    case 7: scatter_tt<CONV, 7, REL>(Y, z); break;
-    default: scatter_tt<CONV, 8, REL>(Y, z); break;
-  }
-}
 
-// load two D-buffer rows (10 columns each: x0-1 .. x0+8), zero the image-border column
-__device__ __forceinline__ void load_rows2(float (&z)[2][ZW], uint32_t taddr, int ch) {
-  tmem_ld8(taddr, z[0]);
-  tmem_ld2(taddr + 8, z[0] + 8);
-  tmem_ld8(taddr + TW, z[1]);
-  tmem_ld2(taddr + TW + 8, z[1] + 8);
+struct EpiState {
+  uint32_t row_base;  // TMEM address of D-buffer 0, row s, lane quadrant
+  int db;
+  uint32_t dph;
+  int lane;
+};
+
+// one tap (compile-time T): three single-row TMEM round trips, D released after the last
+template <int CONV, int T>
+__device__ __forceinline__ void epi_tap(EpiState& e, float (&Y)[4][XH], uint64_t* d_full, uint64_t* d_empty) {
+  const uint32_t a = e.row_base + e.db * BAND_PX;
+  float z[16];
+  mbar_wait(&d_full[e.db], e.dph);
+  tc_fence_after();
+  tmem_ld16(a, z);
   tmem_wait_ld();
-#pragma unroll
-  for (int i = 0; i < 2; ++i) {
-    if (ch == 0)
-      z[i][0] = 0.f;  // column -1
-    else
-      z[i][ZW - 1] = 0.f;  // column 16
+  scatter_row<CONV, T, 0>(Y, z);
+  tmem_ld16(a + TW, z);
+  tmem_wait_ld();
+  scatter_row<CONV, T, 1>(Y, z);
+  tmem_ld16(a + 2 * TW, z);
+  tmem_wait_ld();
+  tc_fence_before();
+  __syncwarp();
+  if (e.lane == 0) mbar_arrive(&d_empty[e.db]);  // D buffer free: MMA may refill it
+  if (++e.db == NDB) {
+    e.db = 0;
+    e.dph ^= 1;
   }
+  scatter_row<CONV, T, 2>(Y, z);
 }
 
-// Epilogue warp: lane quadrant q (co = q*32 + lane), sub-tile rp (output rows 2rp, 2rp+1 of
-// the band) x ch (columns 8ch .. 8ch+7).  Per tap two TMEM round trips of two rows each.
+// Epilogue warp: lane quadrant q (co = q*32 + lane), sub-tile s = output row 4k + s.
 template <int CONV>
 __device__ void epilogue(const TcParams& p, uint32_t tmem, uint64_t* d_full, uint64_t* d_empty) {
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int q = warp % 4;
   const int sub = (warp - EPI_WARP0) / 4;
-  const int rp = sub >> 1, ch = sub & 1;
-  const int x0 = ch * XH;
   const int co_l = q * 32 + lane;
-  const uint32_t lane_base = tmem + ((uint32_t)(q * 32) << 16) + D0 + 2 * rp * TW + x0 - 1;
-  int db = 0;
-  uint32_t dph = 0;
-  float Y[2][4][XH];
+  EpiState e{tmem + ((uint32_t)(q * 32) << 16) + D0 + sub * TW, 0, 0, lane};
+  float Y[4][XH];
   for (int item = blockIdx.x; item < p.items; item += gridDim.x) {
     const int ct = item / p.N, n = item % p.N;
     const int co = ct * 128 + co_l;
     for (int b = 0; b < p.NB; ++b)
       for (int k = 0; k < p.NBK; ++k) {
 #pragma unroll
-        for (int l = 0; l < 2; ++l)
+        for (int r = 0; r < 4; ++r)
 #pragma unroll
-          for (int r = 0; r < 4; ++r)
-#pragma unroll
-            for (int x = 0; x < XH; ++x) Y[l][r][x] = 0.f;
-#pragma unroll 1
-        for (int t = 0; t < 9; ++t) {
-          const uint32_t a = lane_base + db * BAND_PX;
-          float z[2][ZW];
-          mbar_wait(&d_full[db], dph);
-          tc_fence_after();
-          load_rows2(z, a, ch);
-          scatter<CONV, 0>(Y, z, t);
-          load_rows2(z, a + 2 * TW, ch);
-          tc_fence_before();
-          __syncwarp();
-          if (lane == 0) mbar_arrive(&d_empty[db]);  // D buffer free: MMA may refill it
-          if (++db == NDB) {
-            db = 0;
-            dph ^= 1;
-          }
-          scatter<CONV, 2>(Y, z, t);
-        }
-        if (n < p.N && co < p.Cout) {
-#pragma unroll
-          for (int l = 0; l < 2; ++l) {
-            const int row = OUT_ROWS * k + 2 * rp + l;
-            if (row < p.H) finalize_row(p, Y[l], n, co, b, row, x0);
-          }
-        }
+          for (int x = 0; x < XH; ++x) Y[r][x] = 0.f;
+        epi_tap<CONV, 0>(e, Y, d_full, d_empty);
+        epi_tap<CONV, 1>(e, Y, d_full, d_empty);
+        epi_tap<CONV, 2>(e, Y, d_full, d_empty);
+        epi_tap<CONV, 3>(e, Y, d_full, d_empty);
+        epi_tap<CONV, 4>(e, Y, d_full, d_empty);
+        epi_tap<CONV, 5>(e, Y, d_full, d_empty);
+        epi_tap<CONV, 6>(e, Y, d_full, d_empty);
+        epi_tap<CONV, 7>(e, Y, d_full, d_empty);
+        epi_tap<CONV, 8>(e, Y, d_full, d_empty);
+        const int row = OUT_ROWS * k + sub;
+        if (n < p.N && co < p.Cout && row < p.H && p.ablate != 1) finalize_row(p, Y, n, co, b, row, 0);
       }
   }
 }
@@ -365,8 +339,12 @@ __global__ void __launch_bounds__(THREADS, 1) ri_tc_kernel(const __grid_constant
           for (int st = 0; st < 9 * stages_per_tap; ++st) {
             if (wr.used) mbar_wait(&w_empty[wr.s], wr.ph ^ 1);
             if (elect_one()) {
-              mbar_arrive_expect_tx(&w_full[wr.s], stage_bytes);
-              bulk_g2s(ws + wr.s * stage_bytes, wsrc + (size_t)st * stage_bytes, stage_bytes, &w_full[wr.s]);
+              if (p.ablate == 3) {
+                mbar_arrive(&w_full[wr.s]);  // profiling: no weight traffic
+              } else {
+                mbar_arrive_expect_tx(&w_full[wr.s], stage_bytes);
+                bulk_g2s(ws + wr.s * stage_bytes, wsrc + (size_t)st * stage_bytes, stage_bytes, &w_full[wr.s]);
+              }
             }
             __syncwarp();
             wr.adv(S);
@@ -398,7 +376,7 @@ __global__ void __launch_bounds__(THREADS, 1) ri_tc_kernel(const __grid_constant
               tc_fence_after();
               if (elect_one()) {
                 const uint32_t wbase = smem_u32(ws + wr.s * stage_bytes);
-                for (int cl = 0; cl < p.spc; ++cl) {
+                for (int cl = 0; cl < (p.ablate >= 2 ? 0 : p.spc); ++cl) {
                   const int c = sp * p.spc + cl;
                   const uint64_t bh = desc_k_sw128(xaddr + c * XTILE);
                   const uint64_t ah = desc_k_sw128(wbase + cl * parts * WTILE);
@@ -619,6 +597,10 @@ int launch_tc(const rc_desc& d, const float* x, const void* bank, const float* b
   p.spc = plan.spc;
   p.x_bufs = plan.x_bufs;
   p.items = g.NCT * d.n;
+  {
+    const char* ab = getenv("RC_TC_ABLATE");  // profiling switch, see TcParams::ablate
+    p.ablate = ab ? atoi(ab) : 0;
+  }
   int dev, sms;
   RC_CUDA(cudaGetDevice(&dev));
   RC_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));

@@ -50,9 +50,21 @@ __global__ void __launch_bounds__(64, 1)
   __syncthreads();
   if (mc) cluster_sync();
   const size_t tiles_in_region = region / TILE;
-  const size_t start = mode == 0 ? (size_t)blockIdx.x * 37 : 0;
+  const size_t start = (mode == 0 || mode == 4) ? (size_t)blockIdx.x * 37 : 0;
   long long t0 = clock64();
-  if (tid == 0) {
+  if (mode == 4 && tid < 32) {
+    // each stage issued as 4 sub-copies from 4 different lanes
+    for (int i = 0; i < ntiles; ++i) {
+      const int s = i % STAGES;
+      const uint32_t ph = (i / STAGES) & 1;
+      if (i >= STAGES) mbar_wait(&empty[s], ph ^ 1);
+      if (tid == 0) mbar_arrive_expect_tx(&full[s], TILE);
+      __syncwarp();
+      const uint8_t* g = src + ((start + i) % tiles_in_region) * TILE;
+      if (tid < 4) bulk_g2s(smem + s * TILE + tid * (TILE / 4), g + tid * (TILE / 4), TILE / 4, &full[s]);
+      __syncwarp();
+    }
+  } else if (tid == 0) {
     for (int i = 0; i < ntiles; ++i) {
       const int s = i % STAGES;
       const uint32_t ph = (i / STAGES) & 1;
@@ -137,9 +149,10 @@ int main() {
   int sms;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
   run<16384, 4>(src, region, cyc, sms, 1, 0);
-  run<32768, 4>(src, region, cyc, sms, 1, 0);
   run<65536, 3>(src, region, cyc, sms, 1, 0);
-  run<98304, 2>(src, region, cyc, sms, 1, 0);
-  run<65536, 2>(src, region, cyc, sms, 1, 1);
+  run<65536, 3>(src, region, cyc, sms, 1, 4);
+  run<32768, 6>(src, region, cyc, sms, 1, 4);
+  run<16384, 8>(src, region, cyc, sms, 1, 4);
+  run<65536, 2>(src, region, cyc, sms, 1, 4);
   return 0;
 }

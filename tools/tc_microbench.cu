@@ -59,6 +59,33 @@ __global__ void __launch_bounds__(128, 1)
   if (warp == 0) tmem_dealloc<512>(tbase);
 }
 
+template <int NCOL>
+__device__ __forceinline__ float ldtm_sum(uint32_t taddr) {
+  uint32_t r[32];
+  if constexpr (NCOL == 2)
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x2.b32 {%0,%1}, [%2];\n" : "=r"(r[0]), "=r"(r[1]) : "r"(taddr));
+  else if constexpr (NCOL == 8)
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];\n"
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+                 : "r"(taddr));
+  else if constexpr (NCOL == 16) {
+    float v[16];
+    tmem_ld16(taddr, v);
+    for (int i = 0; i < 16; ++i) r[i] = __float_as_uint(v[i]);
+  } else {
+    float v[32];
+    tmem_ld32(taddr, v);
+    for (int i = 0; i < 32; ++i) r[i] = __float_as_uint(v[i]);
+  }
+  tmem_wait_ld();
+  float acc = 0.f;
+#pragma unroll
+  for (int i = 0; i < NCOL; ++i) acc += __uint_as_float(r[i]);
+  return acc;
+}
+
+// TMEM -> RF: each warp issues LOADS back-to-back loads of NCOL columns, then one wait
+template <int NCOL, int LOADS>
 __global__ void ld_bench(int reps, float* sink, long long* cycles) {
   __shared__ uint32_t tbase;
   const int tid = threadIdx.x, warp = tid / 32;
@@ -70,14 +97,10 @@ __global__ void ld_bench(int reps, float* sink, long long* cycles) {
   float acc = 0.f;
   __syncthreads();
   long long t0 = clock64();
-  for (int r = 0; r < reps; ++r)
-    for (int c = (warp / 4) * 32; c < 512; c += 32 * (blockDim.x / 128)) {
-      float v[32];
-      tmem_ld32(base + c, v);
-      tmem_wait_ld();
+  for (int r = 0; r < reps; ++r) {
 #pragma unroll
-      for (int j = 0; j < 32; ++j) acc += v[j];
-    }
+    for (int l = 0; l < LOADS; ++l) acc += ldtm_sum<NCOL>(base + ((r * LOADS + l) * NCOL + warp * 3) % (512 - NCOL));
+  }
   __syncthreads();
   long long t1 = clock64();
   sink[tid] = acc;
@@ -139,19 +162,20 @@ void run_mma() {
   cudaFree(dA); cudaFree(dB); cudaFree(dout); cudaFree(dcyc);
 }
 
+template <int NCOL>
 void run_ld(int warps) {
   float* sink;
   long long* dcyc;
   CK(cudaMalloc(&sink, 4096 * 4));
   CK(cudaMalloc(&dcyc, 8));
-  const int reps = 200;
-  ld_bench<<<1, warps * 32>>>(reps, sink, dcyc);
+  const int reps = 2000;
+  ld_bench<NCOL, 1><<<1, warps * 32>>>(reps, sink, dcyc);
   CK(cudaDeviceSynchronize());
   long long cyc;
   CK(cudaMemcpy(&cyc, dcyc, 8, cudaMemcpyDeviceToHost));
-  const double bytes = (double)reps * 128 * 512 * 4;  // every lane x column read once per rep
-  printf("{\"test\":\"tmem_ld_32x32b_x32\",\"warps\":%d,\"cycles\":%lld,\"bytes_per_cycle\":%.1f}\n", warps,
-         cyc, bytes / cyc);
+  const double bytes = (double)reps * warps * 32 * NCOL * 4;
+  printf("{\"test\":\"tmem_ld_roundtrip\",\"cols\":%d,\"warps\":%d,\"cycles_per_load_per_warp\":%.1f,"
+         "\"bytes_per_cycle\":%.1f}\n", NCOL, warps, (double)cyc / reps, bytes / cyc);
   cudaFree(sink); cudaFree(dcyc);
 }
 
@@ -160,8 +184,11 @@ int main() {
   run_mma<64>();
   run_mma<128>();
   run_mma<256>();
-  run_ld(4);
-  run_ld(8);
-  run_ld(16);
+  run_ld<2>(16);
+  run_ld<8>(16);
+  run_ld<16>(16);
+  run_ld<32>(16);
+  run_ld<8>(4);
+  run_ld<16>(4);
   return 0;
 }
