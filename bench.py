@@ -293,7 +293,8 @@ def main():
             "e2e": {"value": e2e_val, "unit": "TFLOP/s", "h2d_bytes_per_step": int(h2d),
                     "d2h_bytes_per_step": int(d2h), "ms_per_step": e2e_s.item() * 1e3,
                     "path": "rc_ri_conv_forward_host (C-ABI, pinned host buffers)"},
-            "gpu_launches": args.steps,
+            "gpu_launches": args.steps * (2 if desc.kernel_name().startswith("tc_") else 1),
+            "gpu_launches_note": "per step: tc path = x_pack_kernel + ri_tc_kernel; SIMT = one fused kernel",
             "cpu_baseline": cpu,
             "timed_output_matches_e2e": bool(ok),
         }

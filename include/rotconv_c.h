@@ -102,6 +102,11 @@ int rc_bank_precompute(const rc_desc* d, const float* d_w0, const float* d_w1, v
  * [R][Cout][Cin][K][K] floats, from a precomputed bank. */
 int rc_orientation_bank(const rc_desc* d, const void* d_bank, float* d_kernels, void* stream);
 
+/* steer at an arbitrary angle: out = sin(theta)*f_x + cos(theta)*f_y
+ * elementwise over `count` floats, coefficients rounded once from double, no FMA. */
+int rc_steer(const float* d_fx, const float* d_fy, size_t count, double theta, float* d_out,
+             void* stream);
+
 /* ---- the fused layer forward --------------------------------------------
  * Replaces tiled_scatter_conv (scatter_conv.hpp:330-368; R = 1) and the
  * SPEC-defined group_conv_scatter_reuse + orientation_pool_{avg,max} /
@@ -128,6 +133,26 @@ int rc_orientation_pool(int n, int c_out, int r, int h, int w, int pool, int poo
 int rc_ri_conv_forward_host(const rc_desc* d, const float* h_x, const float* h_w0,
                             const float* h_w1, const float* h_bias, float* h_y,
                             uint8_t* h_argmax, int device);
+/* steer with host buffers. */
+int rc_steer_host(const float* h_fx, const float* h_fy, size_t count, double theta, float* h_out,
+                  int device);
+/* build_orientation_bank / transform_kernel with host buffers:
+ * h_kernels receives R*Cout*Cin*K*K floats, orbit-major (o = b*4 + r). */
+int rc_orientation_bank_host(const rc_desc* d, const float* h_w0, const float* h_w1,
+                             float* h_kernels, int device);
+/* orientation_pool_avg / orientation_pool_max / subgroup_pool_max on a
+ * host OrientedFeature batch (N, Cout, R, H, W). */
+int rc_orientation_pool_host(int n, int c_out, int r, int h, int w, int pool, int pool_group,
+                             const float* h_f, const float* h_bias, float* h_y,
+                             uint8_t* h_argmax, int device);
+/* Batch-sharded multi-GPU layer forward (no reference counterpart: the reference loops
+ * over images on one host).  Images are split into contiguous shards
+ * (rc_shard_range) over `n_devices` GPUs (`devices` = NULL means 0..n_devices-1), one
+ * host thread per GPU; each GPU builds the same bank and writes its shard straight into
+ * its slice of h_y / h_argmax.  No collective is involved. */
+int rc_mgpu_forward_host(const rc_desc* d, const float* h_x, const float* h_w0,
+                         const float* h_w1, const float* h_bias, float* h_y, uint8_t* h_argmax,
+                         int n_devices, const int* devices);
 /* tiled_scatter_conv drop-in (scatter_conv.hpp:330-368) for float: validates
  * exactly like the reference (channel mismatch, square kernel, tile dims,
  * halo == K/2, workers >= 1) and returns the identical-semantics output for one

@@ -45,6 +45,11 @@ SIGNATURES = {
     "rc_kernel_name": (C.c_char_p, [_D]),
     "rc_orientation_pool": (C.c_int, [C.c_int] * 7 + [_VP, _VP, _VP, _VP, _VP]),
     "rc_ri_conv_forward_host": (C.c_int, [_D, _VP, _VP, _VP, _VP, _VP, _VP, C.c_int]),
+    "rc_steer": (C.c_int, [_VP, _VP, C.c_size_t, C.c_double, _VP, _VP]),
+    "rc_steer_host": (C.c_int, [_VP, _VP, C.c_size_t, C.c_double, _VP, C.c_int]),
+    "rc_orientation_bank_host": (C.c_int, [_D, _VP, _VP, _VP, C.c_int]),
+    "rc_orientation_pool_host": (C.c_int, [C.c_int] * 7 + [_VP, _VP, _VP, _VP, C.c_int]),
+    "rc_mgpu_forward_host": (C.c_int, [_D, _VP, _VP, _VP, _VP, _VP, _VP, C.c_int, _P(C.c_int)]),
     "rc_tiled_scatter_conv_host": (C.c_int, [_VP] + [C.c_int] * 3 + [_VP] + [C.c_int] * 9 +
                                    [_VP, _P(C.c_ulonglong), _P(C.c_ulonglong),
                                     _P(C.c_ulonglong), C.c_int]),

@@ -76,6 +76,14 @@ __global__ void orient_bank_kernel(const float* __restrict__ bases, float* __res
   }
 }
 
+// steer at an arbitrary angle: same rounding as bank_kernel
+__global__ void steer_kernel(const float* __restrict__ fx, const float* __restrict__ fy, float* __restrict__ out,
+                             long long count, float sn, float cs) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < count;
+       i += (long long)gridDim.x * blockDim.x)
+    out[i] = __fadd_rn(__fmul_rn(sn, fx[i]), __fmul_rn(cs, fy[i]));
+}
+
 int grid_for(long long work, int block) {
   long long g = (work + block - 1) / block;
   if (g > 148LL * 16) g = 148LL * 16;
@@ -104,6 +112,14 @@ int launch_bank(const rc_desc& d, const float* w0, const float* w1, void* bank, 
   if (L.tc_bytes)  // tcgen05 operand tiles (bf16 hi/lo, SW128) from the fp32 bases
     return launch_tc_wpack(d, reinterpret_cast<const float*>(base + L.bases_off),
                            reinterpret_cast<uint8_t*>(base + L.tc_off), s);
+  return RC_OK;
+}
+
+int launch_steer(const float* fx, const float* fy, size_t count, double theta, float* out, cudaStream_t s) {
+  if (count == 0) return RC_OK;
+  steer_kernel<<<grid_for((long long)count, 256), 256, 0, s>>>(fx, fy, out, (long long)count,
+                                                               (float)std::sin(theta), (float)std::cos(theta));
+  RC_CUDA(cudaGetLastError());
   return RC_OK;
 }
 

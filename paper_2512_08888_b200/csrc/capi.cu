@@ -5,6 +5,7 @@
 #include <cstdio>
 #include <cstring>
 #include <mutex>
+#include <thread>
 #include <string>
 #include <vector>
 
@@ -322,6 +323,142 @@ int rc_ri_conv_forward_host(const rc_desc* d, const float* h_x, const float* h_w
   RC_CUDA(cudaMemcpyAsync(h_y, dy, yb, cudaMemcpyDeviceToHost, s));
   if (has_arg) RC_CUDA(cudaMemcpyAsync(h_argmax, da, ab, cudaMemcpyDeviceToHost, s));
   RC_CUDA(cudaStreamSynchronize(s));
+  return RC_OK;
+}
+
+int rc_steer(const float* d_fx, const float* d_fy, size_t count, double theta, float* d_out, void* stream) {
+  if (count > 0 && (!d_fx || !d_fy || !d_out)) return fail(RC_ERR_INVALID, "steer: null pointer");
+  return launch_steer(d_fx, d_fy, count, theta, d_out, static_cast<cudaStream_t>(stream));
+}
+
+int rc_steer_host(const float* h_fx, const float* h_fy, size_t count, double theta, float* h_out, int device) {
+  if (device < 0 || device >= 64) return fail(RC_ERR_INVALID, "steer: bad device");
+  if (count == 0) return RC_OK;
+  if (!h_fx || !h_fy || !h_out) return fail(RC_ERR_INVALID, "steer: null pointer");
+  DeviceGuard guard(device);
+  DeviceCache& c = g_cache[device];
+  std::lock_guard<std::mutex> lock(c.mu);
+  if (!c.stream) RC_CUDA(cudaStreamCreateWithFlags(&c.stream, cudaStreamNonBlocking));
+  const size_t b = count * sizeof(float);
+  void* dx = c.get(0, b);
+  void* dy = c.get(1, b);
+  void* dout = c.get(2, b);
+  if (!dx || !dy || !dout) return fail(RC_ERR_CUDA, "steer: device allocation failed");
+  cudaStream_t s = c.stream;
+  RC_CUDA(cudaMemcpyAsync(dx, h_fx, b, cudaMemcpyHostToDevice, s));
+  RC_CUDA(cudaMemcpyAsync(dy, h_fy, b, cudaMemcpyHostToDevice, s));
+  int st = launch_steer((const float*)dx, (const float*)dy, count, theta, (float*)dout, s);
+  if (st != RC_OK) return st;
+  RC_CUDA(cudaMemcpyAsync(h_out, dout, b, cudaMemcpyDeviceToHost, s));
+  RC_CUDA(cudaStreamSynchronize(s));
+  return RC_OK;
+}
+
+int rc_orientation_bank_host(const rc_desc* d, const float* h_w0, const float* h_w1, float* h_kernels,
+                             int device) {
+  RC_CHECK_DESC(d);
+  if (device < 0 || device >= 64) return fail(RC_ERR_INVALID, "orientation_bank: bad device");
+  if (!h_w0 || !h_kernels || (d->group == RC_GROUP_STEER && !h_w1))
+    return fail(RC_ERR_INVALID, "orientation_bank: null pointer");
+  DeviceGuard guard(device);
+  DeviceCache& c = g_cache[device];
+  std::lock_guard<std::mutex> lock(c.mu);
+  if (!c.stream) RC_CUDA(cudaStreamCreateWithFlags(&c.stream, cudaStreamNonBlocking));
+  const size_t wb = (size_t)d->c_out * d->c_in * d->k * d->k * sizeof(float);
+  const size_t kb = wb * (size_t)num_bases(*d) * rot_per_base(*d);
+  void* dw0 = c.get(1, wb);
+  void* dw1 = d->group == RC_GROUP_STEER ? c.get(2, wb) : nullptr;
+  void* dbank = c.get(4, bank_layout(*d).total);
+  void* dk = c.get(5, kb);
+  if (!dw0 || !dbank || !dk || (d->group == RC_GROUP_STEER && !dw1))
+    return fail(RC_ERR_CUDA, "orientation_bank: device allocation failed");
+  cudaStream_t s = c.stream;
+  RC_CUDA(cudaMemcpyAsync(dw0, h_w0, wb, cudaMemcpyHostToDevice, s));
+  if (dw1) RC_CUDA(cudaMemcpyAsync(dw1, h_w1, wb, cudaMemcpyHostToDevice, s));
+  int st = launch_bank(*d, (const float*)dw0, (const float*)dw1, dbank, s);
+  if (st != RC_OK) return st;
+  st = launch_orientation_bank(*d, dbank, (float*)dk, s);
+  if (st != RC_OK) return st;
+  RC_CUDA(cudaMemcpyAsync(h_kernels, dk, kb, cudaMemcpyDeviceToHost, s));
+  RC_CUDA(cudaStreamSynchronize(s));
+  return RC_OK;
+}
+
+int rc_orientation_pool_host(int n, int c_out, int r, int h, int w, int pool, int pool_group,
+                             const float* h_f, const float* h_bias, float* h_y, uint8_t* h_argmax,
+                             int device) {
+  if (n < 0 || c_out < 1 || r < 1 || h < 1 || w < 1)
+    return fail(RC_ERR_INVALID, "OrientedFeature: dimensions must be positive");
+  if (pool == RC_POOL_SUBGROUP && (pool_group < 1 || r % pool_group != 0))
+    return fail(RC_ERR_INVALID, "subgroup_pool_max: R not divisible by group_size");
+  if (pool < RC_POOL_NONE || pool > RC_POOL_SUBGROUP) return fail(RC_ERR_INVALID, "ri_conv: unknown pool");
+  if (device < 0 || device >= 64) return fail(RC_ERR_INVALID, "orientation_pool: bad device");
+  if (n == 0) return RC_OK;
+  const int gf = pool == RC_POOL_SUBGROUP ? pool_group : (pool == RC_POOL_NONE ? 1 : r);
+  const size_t plane = (size_t)h * w;
+  const size_t fb = (size_t)n * c_out * r * plane * sizeof(float);
+  const size_t yb = (size_t)n * c_out * (r / gf) * plane * sizeof(float);
+  const bool has_arg = h_argmax && pool != RC_POOL_AVG;
+  DeviceGuard guard(device);
+  DeviceCache& c = g_cache[device];
+  std::lock_guard<std::mutex> lock(c.mu);
+  if (!c.stream) RC_CUDA(cudaStreamCreateWithFlags(&c.stream, cudaStreamNonBlocking));
+  void* df = c.get(0, fb);
+  void* dbias = h_bias ? c.get(3, c_out * sizeof(float)) : nullptr;
+  void* dy = c.get(5, yb);
+  void* da = has_arg ? c.get(6, yb / sizeof(float)) : nullptr;
+  if (!df || !dy || (h_bias && !dbias) || (has_arg && !da))
+    return fail(RC_ERR_CUDA, "orientation_pool: device allocation failed");
+  cudaStream_t s = c.stream;
+  RC_CUDA(cudaMemcpyAsync(df, h_f, fb, cudaMemcpyHostToDevice, s));
+  if (dbias) RC_CUDA(cudaMemcpyAsync(dbias, h_bias, c_out * sizeof(float), cudaMemcpyHostToDevice, s));
+  int st = launch_pool(n, c_out, r, h, w, pool, pool_group, (const float*)df, (const float*)dbias, (float*)dy,
+                       (uint8_t*)da, s);
+  if (st != RC_OK) return st;
+  RC_CUDA(cudaMemcpyAsync(h_y, dy, yb, cudaMemcpyDeviceToHost, s));
+  if (has_arg) RC_CUDA(cudaMemcpyAsync(h_argmax, da, yb / sizeof(float), cudaMemcpyDeviceToHost, s));
+  RC_CUDA(cudaStreamSynchronize(s));
+  return RC_OK;
+}
+
+// Batch-sharded multi-GPU forward: contiguous shards (rc_shard_range), one
+// host thread per device; every device builds the same bank from the same weights and
+// each shard lands directly in its slice of the caller's host output (no collective).
+int rc_mgpu_forward_host(const rc_desc* d, const float* h_x, const float* h_w0, const float* h_w1,
+                         const float* h_bias, float* h_y, uint8_t* h_argmax, int n_devices,
+                         const int* devices) {
+  RC_CHECK_DESC(d);
+  if (n_devices < 1 || n_devices > 64) return fail(RC_ERR_INVALID, "mgpu_forward: need 1..64 devices");
+  int count = 0;
+  RC_CUDA(cudaGetDeviceCount(&count));
+  for (int i = 0; i < n_devices; ++i) {
+    const int dev = devices ? devices[i] : i;
+    if (dev < 0 || dev >= count) return fail(RC_ERR_INVALID, "mgpu_forward: bad device");
+    for (int j = 0; j < i; ++j)
+      if ((devices ? devices[j] : j) == dev) return fail(RC_ERR_INVALID, "mgpu_forward: duplicate device");
+  }
+  const size_t x_img = (size_t)d->c_in * d->h * d->w;
+  const size_t y_img = (size_t)d->c_out * out_orientations(*d) * d->h * d->w;
+  std::vector<int> status(n_devices, RC_OK);
+  std::vector<std::string> msg(n_devices);
+  std::vector<std::thread> workers;
+  for (int i = 0; i < n_devices; ++i) {
+    int b = 0, e = 0;
+    rc_shard_range(d->n, n_devices, i, &b, &e);
+    workers.emplace_back([&, i, b, e] {
+      rc_desc ld = *d;
+      ld.n = e - b;
+      const int dev = devices ? devices[i] : i;
+      status[i] = rc_ri_conv_forward_host(&ld, h_x + (size_t)b * x_img, h_w0, h_w1, h_bias,
+                                          h_y + (size_t)b * y_img,
+                                          h_argmax ? h_argmax + (size_t)b * y_img : nullptr, dev);
+      if (status[i] != RC_OK) msg[i] = g_err;  // g_err is thread-local: copy it out
+    });
+  }
+  for (auto& t : workers) t.join();
+  for (int i = 0; i < n_devices; ++i)
+    if (status[i] != RC_OK)
+      return fail(status[i], "mgpu_forward: device " + std::to_string(i) + ": " + msg[i]);
   return RC_OK;
 }
 

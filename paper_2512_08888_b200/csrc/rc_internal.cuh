@@ -63,6 +63,7 @@ void slice_tap_offsets(int k, int convention, TapOffsets* out);
 int launch_bank(const rc_desc& d, const float* w0, const float* w1, void* bank,
                 cudaStream_t s);
 int launch_orientation_bank(const rc_desc& d, const void* bank, float* out, cudaStream_t s);
+int launch_steer(const float* fx, const float* fy, size_t count, double theta, float* out, cudaStream_t s);
 // returns RC_ERR_UNSUPPORTED if the SIMT K=3 fast kernel cannot handle d
 int launch_simt_k3(const rc_desc& d, const float* x, const void* bank, const float* bias,
                    float* y, uint8_t* argmax, cudaStream_t s, bool dry_run, const char** name);
