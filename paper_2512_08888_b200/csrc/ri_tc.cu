@@ -38,23 +38,29 @@ namespace {
 
 using namespace tc;
 
-constexpr int TW = 16;                  // image width handled by this kernel
-constexpr int OUT_ROWS = 4;             // output rows per band
-constexpr int IN_ROWS = OUT_ROWS + 2;   // input rows per band (halo above and below)
-constexpr int BAND_PX = IN_ROWS * TW;   // 96 = N of the MMA
+// Band geometry per image width TW (16 or 32): a band is OUT_ROWS output rows (64 output
+// pixels, the register budget of the epilogue) computed from IN_ROWS = OUT_ROWS + 2 input
+// rows; every epilogue thread owns 16 pixels (one row of TW = 16, half a row of TW = 32).
+template <int TW>
+struct Geo {
+  static constexpr int OUT_ROWS = 64 / TW;               // 4 | 2
+  static constexpr int IN_ROWS = OUT_ROWS + 2;           // 6 | 4
+  static constexpr int BAND_PX = IN_ROWS * TW;           // 96 | 128 = N of the MMA
+  static constexpr int XTILE = BAND_PX * 64 * 2;         // bytes of one [BAND_PX x 64 ci] bf16 tile
+  static constexpr int HALVES = TW / 16;                 // epilogue threads per output row
+  static constexpr int NDB = TW == 16 ? 4 : 3;           // TMEM D buffers: 16 + NDB*BAND_PX <= 512
+};
 constexpr int KC = 64;                  // ci per chunk (one 128-byte swizzle row of bf16)
-constexpr int XTILE = BAND_PX * KC * 2;  // 12 KB
 constexpr int WTILE = 128 * KC * 2;      // 16 KB
 constexpr int NUM_EPI = 16;              // epilogue warps (4 warpgroups)
 constexpr int EPI_WARP0 = 4;             // warps 0-3: producer warpgroup (TMA, MMA, 2 idle)
 constexpr int THREADS = 32 * (EPI_WARP0 + NUM_EPI);
 constexpr int REGS_PRODUCER = 32;        // setmaxnreg budgets: 20 warps x 96 at launch
 constexpr int REGS_EPILOGUE = 112;
-constexpr int NDB = 4;                   // TMEM accumulator buffers (MMA <-> epilogue)
+constexpr int MAX_NDB = 4;
 constexpr uint32_t D0 = 16;              // D buffers from column 16: the 1-column-left halo
-                                         // load of a row stays inside the allocation
-constexpr int XH = TW;                   // output columns per epilogue thread (a full row)
-// TMEM columns: 16 + 4 * 96 = 400 <= 512
+                                         // load of a band's first pixel stays in the allocation
+constexpr int XH = 16;                   // output columns per epilogue thread
 
 struct TcParams {
   const uint8_t* xh;  // packed X tiles [n][band][chunk] (hi), 12 KB each
@@ -65,7 +71,8 @@ struct TcParams {
   uint8_t* am;
   int N, H, Cout, NB, NBK, NC, NCT, pool, gf, RO, passes, w_stages, spc, x_bufs, items;
   float inv_r;  // 1/R for average pooling (R a power of two)
-  int ablate;   // profiling only: 1 = skip epilogue math, 2 = skip MMAs, 3 = skip MMAs + W loads
+  int ablate;   // profiling only: 1 = skip stores, 2 = skip MMAs, 3 = skip MMAs + W loads,
+                // 4 = skip W loads (MMAs on stale tiles), 5 = epilogue skips TMEM loads + scatter
 };
 
 // ---- TMEM -> registers ----------------------------------------------------------------
@@ -116,6 +123,7 @@ __device__ __forceinline__ void store_row(const TcParams& p, size_t off, float (
 // pool + bias + store one output row (16 px) of base b; same semantics as ri_simt.cu.
 // Fold groups gf in {1, 2, 4} stay inside a base; gf % 4 == 0 spans bases through a
 // partial (value, argmax) kept in the output row itself (same thread, program order).
+template <int TW>
 __device__ __forceinline__ void finalize_row(const TcParams& p, float (&Yr)[4][XH], int n, int co, int b,
                                              int row, int x0) {
   const size_t plane = (size_t)p.H * TW;
@@ -175,11 +183,13 @@ __device__ __forceinline__ void finalize_row(const TcParams& p, float (&Yr)[4][X
 }
 
 // ---- scatter ------------------------------------------------------------------------
-// Output row o = 4k + s of warp sub-tile s reads D-buffer rows s .. s+2 (input rows o-1 ..
-// o+1).  Y_r(p) += Z_t(p + (di, dj)): for tap T and rotation r the single contributing row
-// is I = 1 + di; columns x + dj outside [0, 16) are the zero padding and are skipped.
-template <int CONV, int T, int I>
-__device__ __forceinline__ void scatter_row(float (&Y)[4][XH], const float (&z)[16]) {
+// A thread's 16 output columns [x0, x0+16) of output row o read input rows o-1 .. o+1
+// (D-buffer rows s .. s+2).  z[c] holds input column x0 - 1 + c (c = 0..17); columns
+// outside the image were loaded as 0 (TW = 32) or are skipped at compile time (TW = 16:
+// the thread's 16 columns are the whole row).  Y_r(p) += Z_t(p + (di, dj)): for tap T and
+// rotation r the single contributing row is I = 1 + di.
+template <int TW, int CONV, int T, int I>
+__device__ __forceinline__ void scatter_row(float (&Y)[4][XH], const float (&z)[18]) {
 #pragma unroll
   for (int r = 0; r < 4; ++r) {
     const int di = make_k3(CONV).di[r][T];
@@ -187,35 +197,57 @@ __device__ __forceinline__ void scatter_row(float (&Y)[4][XH], const float (&z)[
     if (1 + di != I) continue;
 #pragma unroll
     for (int x = 0; x < XH; ++x) {
-      const int src = x + dj;
-      if (src < 0 || src >= TW) continue;
+      const int src = x + dj + 1;
+      if (TW == 16 && (src < 1 || src > 16)) continue;
       Y[r][x] += z[src];
     }
   }
 }
 
+__device__ __forceinline__ float tmem_ld1(uint32_t taddr) {
+  uint32_t r;
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x1.b32 {%0}, [%1];\n" : "=r"(r) : "r"(taddr));
+  return __uint_as_float(r);
+}
+
+// one input row of the thread's window: 16 columns + (TW = 32) the two halo columns
+template <int TW>
+__device__ __forceinline__ void load_row(uint32_t a, int half, float (&z)[18]) {
+  float v[16];
+  tmem_ld16(a, v);
+  if (TW == 32) {
+    z[0] = tmem_ld1(a - 1);
+    z[17] = tmem_ld1(a + 16);
+  }
+  tmem_wait_ld();
+#pragma unroll
+  for (int i = 0; i < 16; ++i) z[1 + i] = v[i];
+  if (TW == 32) {  // image edges: the neighbouring half does not exist
+    if (half == 0) z[0] = 0.f;
+    if (half == TW / 16 - 1) z[17] = 0.f;
+  }
+}
+
 struct EpiState {
-  uint32_t row_base;  // TMEM address of D-buffer 0, row s, lane quadrant
+  uint32_t row_base;  // TMEM address of D-buffer 0, first input row of the thread, its columns
   int db;
   uint32_t dph;
-  int lane;
+  int lane, half;
 };
 
 // one tap (compile-time T): three single-row TMEM round trips, D released after the last
-template <int CONV, int T>
+template <int TW, int CONV, int T>
 __device__ __forceinline__ void epi_tap(EpiState& e, float (&Y)[4][XH], uint64_t* d_full, uint64_t* d_empty) {
-  const uint32_t a = e.row_base + e.db * BAND_PX;
-  float z[16];
+  constexpr int NDB = Geo<TW>::NDB;
+  const uint32_t a = e.row_base + e.db * Geo<TW>::BAND_PX;
+  float z[18];
   mbar_wait(&d_full[e.db], e.dph);
   tc_fence_after();
-  tmem_ld16(a, z);
-  tmem_wait_ld();
-  scatter_row<CONV, T, 0>(Y, z);
-  tmem_ld16(a + TW, z);
-  tmem_wait_ld();
-  scatter_row<CONV, T, 1>(Y, z);
-  tmem_ld16(a + 2 * TW, z);
-  tmem_wait_ld();
+  load_row<TW>(a, e.half, z);
+  scatter_row<TW, CONV, T, 0>(Y, z);
+  load_row<TW>(a + TW, e.half, z);
+  scatter_row<TW, CONV, T, 1>(Y, z);
+  load_row<TW>(a + 2 * TW, e.half, z);
   tc_fence_before();
   __syncwarp();
   if (e.lane == 0) mbar_arrive(&d_empty[e.db]);  // D buffer free: MMA may refill it
@@ -223,38 +255,53 @@ __device__ __forceinline__ void epi_tap(EpiState& e, float (&Y)[4][XH], uint64_t
     e.db = 0;
     e.dph ^= 1;
   }
-  scatter_row<CONV, T, 2>(Y, z);
+  scatter_row<TW, CONV, T, 2>(Y, z);
 }
 
-// Epilogue warp: lane quadrant q (co = q*32 + lane), sub-tile s = output row 4k + s.
-template <int CONV>
+// Epilogue warp: lane quadrant q (co = q*32 + lane); sub-tile sub = (output row of the
+// band, column half): TW = 16 -> 4 rows x 1 half, TW = 32 -> 2 rows x 2 halves.
+template <int TW, int CONV>
 __device__ void epilogue(const TcParams& p, uint32_t tmem, uint64_t* d_full, uint64_t* d_empty) {
+  using G = Geo<TW>;
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int q = warp % 4;
   const int sub = (warp - EPI_WARP0) / 4;
+  const int srow = sub / G::HALVES, half = sub % G::HALVES;
   const int co_l = q * 32 + lane;
-  EpiState e{tmem + ((uint32_t)(q * 32) << 16) + D0 + sub * TW, 0, 0, lane};
+  EpiState e{tmem + ((uint32_t)(q * 32) << 16) + D0 + srow * TW + half * 16, 0, 0, lane, half};
   float Y[4][XH];
   for (int item = blockIdx.x; item < p.items; item += gridDim.x) {
-    const int ct = item / p.N, n = item % p.N;
+    const int n = item / p.NCT, ct = item % p.NCT;
     const int co = ct * 128 + co_l;
+    if (p.ablate == 5) {  // profiling: consume D buffers without reading them
+      for (int i = 0; i < p.NB * p.NBK * 9; ++i) {
+        mbar_wait(&d_full[e.db], e.dph);
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&d_empty[e.db]);
+        if (++e.db == G::NDB) {
+          e.db = 0;
+          e.dph ^= 1;
+        }
+      }
+      continue;
+    }
     for (int b = 0; b < p.NB; ++b)
       for (int k = 0; k < p.NBK; ++k) {
 #pragma unroll
         for (int r = 0; r < 4; ++r)
 #pragma unroll
           for (int x = 0; x < XH; ++x) Y[r][x] = 0.f;
-        epi_tap<CONV, 0>(e, Y, d_full, d_empty);
-        epi_tap<CONV, 1>(e, Y, d_full, d_empty);
-        epi_tap<CONV, 2>(e, Y, d_full, d_empty);
-        epi_tap<CONV, 3>(e, Y, d_full, d_empty);
-        epi_tap<CONV, 4>(e, Y, d_full, d_empty);
-        epi_tap<CONV, 5>(e, Y, d_full, d_empty);
-        epi_tap<CONV, 6>(e, Y, d_full, d_empty);
-        epi_tap<CONV, 7>(e, Y, d_full, d_empty);
-        epi_tap<CONV, 8>(e, Y, d_full, d_empty);
-        const int row = OUT_ROWS * k + sub;
-        if (n < p.N && co < p.Cout && row < p.H && p.ablate != 1) finalize_row(p, Y, n, co, b, row, 0);
+        epi_tap<TW, CONV, 0>(e, Y, d_full, d_empty);
+        epi_tap<TW, CONV, 1>(e, Y, d_full, d_empty);
+        epi_tap<TW, CONV, 2>(e, Y, d_full, d_empty);
+        epi_tap<TW, CONV, 3>(e, Y, d_full, d_empty);
+        epi_tap<TW, CONV, 4>(e, Y, d_full, d_empty);
+        epi_tap<TW, CONV, 5>(e, Y, d_full, d_empty);
+        epi_tap<TW, CONV, 6>(e, Y, d_full, d_empty);
+        epi_tap<TW, CONV, 7>(e, Y, d_full, d_empty);
+        epi_tap<TW, CONV, 8>(e, Y, d_full, d_empty);
+        const int row = G::OUT_ROWS * k + srow;
+        if (n < p.N && co < p.Cout && row < p.H && p.ablate != 1) finalize_row<TW>(p, Y, n, co, b, row, half * 16);
       }
   }
 }
@@ -272,8 +319,12 @@ struct Ring {
   }
 };
 
-template <int CONV>
+template <int TW, int CONV>
 __global__ void __launch_bounds__(THREADS, 1) ri_tc_kernel(const __grid_constant__ TcParams p) {
+  using G = Geo<TW>;
+  constexpr int NDB = G::NDB;
+  constexpr int XTILE = G::XTILE;
+  constexpr int BAND_PX = G::BAND_PX;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   // 1 KB alignment for the SW128 atoms
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -282,7 +333,7 @@ __global__ void __launch_bounds__(THREADS, 1) ri_tc_kernel(const __grid_constant
   const int XB = p.x_bufs;               // 1 or 2 X band buffers
   uint8_t* xs = smem;
   uint8_t* ws = smem + XB * xbuf_bytes;  // W ring
-  __shared__ uint64_t w_full[8], w_empty[8], x_full[2], x_empty[2], d_full[NDB], d_empty[NDB];
+  __shared__ uint64_t w_full[8], w_empty[8], x_full[2], x_empty[2], d_full[MAX_NDB], d_empty[MAX_NDB];
   __shared__ uint32_t tmem_base_sh;
 
   const int warp = threadIdx.x / 32;
@@ -320,7 +371,7 @@ __global__ void __launch_bounds__(THREADS, 1) ri_tc_kernel(const __grid_constant
     Ring wr;
     uint32_t xc = 0;
     for (int item = blockIdx.x; item < p.items; item += gridDim.x) {
-      const int ct = item / p.N, n = item % p.N;
+      const int n = item / p.NCT, ct = item % p.NCT;
       for (int b = 0; b < p.NB; ++b)
         for (int k = 0; k < p.NBK; ++k) {
           const int xb = XB == 2 ? (xc & 1) : 0;
@@ -339,7 +390,7 @@ __global__ void __launch_bounds__(THREADS, 1) ri_tc_kernel(const __grid_constant
           for (int st = 0; st < 9 * stages_per_tap; ++st) {
             if (wr.used) mbar_wait(&w_empty[wr.s], wr.ph ^ 1);
             if (elect_one()) {
-              if (p.ablate == 3) {
+              if (p.ablate == 3 || p.ablate == 4) {
                 mbar_arrive(&w_full[wr.s]);  // profiling: no weight traffic
               } else {
                 mbar_arrive_expect_tx(&w_full[wr.s], stage_bytes);
@@ -376,7 +427,7 @@ __global__ void __launch_bounds__(THREADS, 1) ri_tc_kernel(const __grid_constant
               tc_fence_after();
               if (elect_one()) {
                 const uint32_t wbase = smem_u32(ws + wr.s * stage_bytes);
-                for (int cl = 0; cl < (p.ablate >= 2 ? 0 : p.spc); ++cl) {
+                for (int cl = 0; cl < ((p.ablate == 2 || p.ablate == 3) ? 0 : p.spc); ++cl) {
                   const int c = sp * p.spc + cl;
                   const uint64_t bh = desc_k_sw128(xaddr + c * XTILE);
                   const uint64_t ah = desc_k_sw128(wbase + cl * parts * WTILE);
@@ -411,7 +462,7 @@ __global__ void __launch_bounds__(THREADS, 1) ri_tc_kernel(const __grid_constant
   } else if (warp >= EPI_WARP0) {
     // ------------------------------------------------------------ epilogue
     asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(REGS_EPILOGUE));
-    epilogue<CONV>(p, tmem, d_full, d_empty);
+    epilogue<TW, CONV>(p, tmem, d_full, d_empty);
   }
   tc_fence_before();
   __syncthreads();
@@ -424,22 +475,25 @@ __device__ __forceinline__ void split_bf16(float v, __nv_bfloat16& hi, __nv_bflo
   lo = __float2bfloat16_rn(v - __bfloat162float(hi));
 }
 
-// X fp32 NCHW (W = 16) -> SW128 bf16 tiles [n][band k][chunk][96 px][64 ci] (hi, lo planes);
-// band k holds input rows 4k-1 .. 4k+4, rows outside the image are zero (the padding).
+// X fp32 NCHW -> SW128 bf16 tiles [n][band k][chunk][BAND_PX px][64 ci] (hi, lo planes);
+// band k holds input rows k*OUT_ROWS-1 .. k*OUT_ROWS+OUT_ROWS; rows outside the image are
+// zero (the padding).
+template <int TW>
 __global__ void x_pack_kernel(const float* __restrict__ x, uint8_t* __restrict__ xh,
                               uint8_t* __restrict__ xl, int Cin, int H, int NBK, int NC) {
-  __shared__ float tile[KC][BAND_PX + 1];
+  using G = Geo<TW>;
+  __shared__ float tile[KC][G::BAND_PX + 1];
   const int c = blockIdx.x, k = blockIdx.y, n = blockIdx.z;
-  for (int i = threadIdx.x; i < KC * BAND_PX; i += blockDim.x) {
-    const int cl = i / BAND_PX, px = i % BAND_PX;
-    const int ci = c * KC + cl, row = k * OUT_ROWS - 1 + px / TW, col = px % TW;
+  for (int i = threadIdx.x; i < KC * G::BAND_PX; i += blockDim.x) {
+    const int cl = i / G::BAND_PX, px = i % G::BAND_PX;
+    const int ci = c * KC + cl, row = k * G::OUT_ROWS - 1 + px / TW, col = px % TW;
     tile[cl][px] = (ci < Cin && row >= 0 && row < H) ? x[(((size_t)n * Cin + ci) * H + row) * TW + col] : 0.f;
   }
   __syncthreads();
   const size_t tidx = ((size_t)n * NBK + k) * NC + c;
-  uint8_t* oh = xh + tidx * XTILE;
-  uint8_t* ol = xl ? xl + tidx * XTILE : nullptr;
-  for (int i = threadIdx.x; i < BAND_PX * (KC / 8); i += blockDim.x) {
+  uint8_t* oh = xh + tidx * G::XTILE;
+  uint8_t* ol = xl ? xl + tidx * G::XTILE : nullptr;
+  for (int i = threadIdx.x; i < G::BAND_PX * (KC / 8); i += blockDim.x) {
     const int px = i / (KC / 8), g = i % (KC / 8);
     __align__(16) __nv_bfloat16 h8[8], l8[8];
 #pragma unroll
@@ -482,15 +536,17 @@ __global__ void w_pack_kernel(const float* __restrict__ bases, uint8_t* __restri
 }
 
 struct TcGeom {
-  int NBK, NC, NCT;
+  int NBK, NC, NCT, xtile;
   size_t x_plane, w_plane;
 };
 TcGeom geom(const rc_desc& d) {
   TcGeom g;
-  g.NBK = (d.h + OUT_ROWS - 1) / OUT_ROWS;
+  const int out_rows = d.w == 32 ? Geo<32>::OUT_ROWS : Geo<16>::OUT_ROWS;
+  g.xtile = d.w == 32 ? Geo<32>::XTILE : Geo<16>::XTILE;
+  g.NBK = (d.h + out_rows - 1) / out_rows;
   g.NC = (d.c_in + KC - 1) / KC;
   g.NCT = (d.c_out + 127) / 128;
-  g.x_plane = (size_t)d.n * g.NBK * g.NC * XTILE;
+  g.x_plane = (size_t)d.n * g.NBK * g.NC * g.xtile;
   g.w_plane = (size_t)num_bases(d) * g.NCT * 9 * g.NC * WTILE;
   return g;
 }
@@ -504,7 +560,7 @@ struct SmemPlan {
 SmemPlan smem_plan(const TcGeom& g, int parts) {
   SmemPlan sp{0, 0, 0, 0};
   const size_t cap = 232448 - 1024 - 1024;  // dynamic smem minus alignment slack / statics
-  const size_t xbuf = (size_t)parts * g.NC * XTILE;
+  const size_t xbuf = (size_t)parts * g.NC * g.xtile;
   const size_t chunk = (size_t)parts * WTILE;
   for (int xb = 2; xb >= 1 && sp.spc == 0; --xb) {
     if (xb * xbuf >= cap) continue;
@@ -531,7 +587,7 @@ bool tc_supported(const rc_desc& d) {
   const int R = d.orientations;
   const bool fold_ok = d.pool == RC_POOL_NONE || (d.pool == RC_POOL_AVG && (R & (R - 1)) == 0) || gf == 1 ||
                        gf == 2 || gf % 4 == 0;
-  if (!(d.k == 3 && d.w == TW && d.group != RC_GROUP_SINGLE && fold_ok &&
+  if (!(d.k == 3 && (d.w == 16 || d.w == 32) && d.group != RC_GROUP_SINGLE && fold_ok &&
         (d.precision == RC_PREC_BF16 || d.precision == RC_PREC_BF16X3 || d.precision == RC_PREC_AUTO)))
     return false;
   const int parts = d.precision == RC_PREC_BF16 ? 1 : 2;
@@ -560,7 +616,10 @@ int launch_tc_wpack(const rc_desc& d, const float* bases, uint8_t* tc_section, c
 int launch_tc(const rc_desc& d, const float* x, const void* bank, const float* bias, float* y, uint8_t* am,
               void* ws, size_t ws_bytes, cudaStream_t s, bool dry_run, const char** name) {
   if (!tc_supported(d)) return RC_ERR_UNSUPPORTED;
-  if (name) *name = d.precision == RC_PREC_BF16 ? "tc_k3w16_bf16" : "tc_k3w16_bf16x3";
+  if (name) {
+    static const char* names[2][2] = {{"tc_k3w16_bf16x3", "tc_k3w16_bf16"}, {"tc_k3w32_bf16x3", "tc_k3w32_bf16"}};
+    *name = names[d.w == 32][d.precision == RC_PREC_BF16];
+  }
   if (dry_run || d.n == 0) return RC_OK;
   const TcGeom g = geom(d);
   if (ws_bytes < tc_workspace_bytes(d) || ws == nullptr)
@@ -569,7 +628,10 @@ int launch_tc(const rc_desc& d, const float* x, const void* bank, const float* b
   const int parts = passes == 3 ? 2 : 1;
   uint8_t* xh = static_cast<uint8_t*>(ws);
   uint8_t* xl = passes == 3 ? xh + g.x_plane : nullptr;
-  x_pack_kernel<<<dim3(g.NC, g.NBK, d.n), 256, 0, s>>>(x, xh, xl, d.c_in, d.h, g.NBK, g.NC);
+  if (d.w == 32)
+    x_pack_kernel<32><<<dim3(g.NC, g.NBK, d.n), 256, 0, s>>>(x, xh, xl, d.c_in, d.h, g.NBK, g.NC);
+  else
+    x_pack_kernel<16><<<dim3(g.NC, g.NBK, d.n), 256, 0, s>>>(x, xh, xl, d.c_in, d.h, g.NBK, g.NC);
   RC_CUDA(cudaGetLastError());
   const BankLayout L = bank_layout(d);
   const uint8_t* tcb = static_cast<const uint8_t*>(bank) + L.tc_off;
@@ -605,7 +667,8 @@ int launch_tc(const rc_desc& d, const float* x, const void* bank, const float* b
   RC_CUDA(cudaGetDevice(&dev));
   RC_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
   const int grid = p.items < sms ? p.items : sms;
-  auto fn = d.convention == RC_CONV_RAW ? ri_tc_kernel<1> : ri_tc_kernel<0>;
+  void (*fn)(TcParams) = d.w == 32 ? (d.convention == RC_CONV_RAW ? ri_tc_kernel<32, 1> : ri_tc_kernel<32, 0>)
+                                    : (d.convention == RC_CONV_RAW ? ri_tc_kernel<16, 1> : ri_tc_kernel<16, 0>);
   RC_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)plan.bytes));
   fn<<<grid, THREADS, plan.bytes, s>>>(p);
   RC_CUDA(cudaGetLastError());

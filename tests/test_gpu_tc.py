@@ -94,6 +94,51 @@ def test_tc_random_tolerance(O, dev, cfg, precision):
         assert np.array_equal(a[safe], a_ref[safe])
 
 
+TC32_CONFIGS = [
+    # (n, cin, h, cout, group, R, pool, g, convention) at W = 32
+    (2, 64, 32, 128, "p4", 4, "subgroup", 4, "scatter"),
+    (2, 128, 7, 256, "p4m", 8, "max", 8, "scatter"),
+    (1, 32, 3, 130, "p4m", 8, "subgroup", 2, "raw"),
+    (2, 64, 32, 128, "p4", 4, "none", 4, "scatter"),
+    (1, 48, 5, 128, "p4m", 8, "avg", 4, "scatter"),
+]
+
+
+@pytest.mark.parametrize("precision", ["bf16", "bf16x3"])
+@pytest.mark.parametrize("cfg", TC32_CONFIGS, ids=lambda c: "-".join(map(str, c)))
+def test_tc_w32_dyadic_bitexact(O, dev, cfg, precision):
+    import paper_2512_08888_b200 as P
+    n, cin, h, cout, g, R, pool, pg, conv = cfg
+    d = O.Desc(n, cin, h, 32, cout, 3, g, R, pool, pg, conv)
+    rng = np.random.default_rng(abs(hash(cfg)) % 2**32)
+    x = dyadic(rng, (n, cin, h, 32))
+    w0 = dyadic(rng, (cout, cin, 3, 3))
+    bias = dyadic(rng, cout)
+    y_ref, a_ref = O.ri_forward(d, x, w0, None, bias)
+    y, a = run(P, d, x, w0, None, bias, precision, dev)
+    assert np.array_equal(y, y_ref), f"max|dy| = {np.abs(y - y_ref).max()}"
+    if a_ref is not None:
+        assert np.array_equal(a, a_ref), f"argmax mismatches {(a != a_ref).sum()}"
+
+
+@pytest.mark.parametrize("precision", ["bf16", "bf16x3"])
+def test_tc_w32_c4_shape_random(O, dev, precision):
+    """C4 layer shape (32x32, 128 -> 512, steer R=16, subgroup-4) on 2 images vs the oracle."""
+    import paper_2512_08888_b200 as P
+    n, cin, h, cout = 2, 128, 32, 512
+    d = O.Desc(n, cin, h, 32, cout, 3, "steer", 16, "subgroup", 4)
+    rng = np.random.default_rng(44)
+    x = rng.uniform(-1, 1, (n, cin, h, 32)).astype(np.float32)
+    s = 1 / np.sqrt(cin * 9)
+    w0 = rng.uniform(-s, s, (cout, cin, 3, 3)).astype(np.float32)
+    w1 = rng.uniform(-s, s, (cout, cin, 3, 3)).astype(np.float32)
+    bias = rng.uniform(-0.1, 0.1, cout).astype(np.float32)
+    y_ref, a_ref = O.ri_forward(d, x, w0, w1, bias, nthreads=8)
+    y, a = run(P, d, x, w0, w1, bias, precision, dev)
+    err = np.abs(y.astype(np.float64) - y_ref).max() / np.abs(y_ref).max()
+    assert err <= TOL[precision], f"normwise {err:.3e}"
+
+
 def test_tc_matches_simt_on_c3_shape_subset(O, dev):
     """C3 layer shape (256 -> 1024, steer R=8, subgroup-4) on 8 images: bf16x3 vs the
     FP32 CUDA-core kernel, normwise, plus determinism."""
