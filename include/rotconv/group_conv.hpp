@@ -63,7 +63,7 @@ enum class Pooling { none = RC_POOL_NONE, avg = RC_POOL_AVG, max = RC_POOL_MAX, 
 namespace detail {
 
 inline rc_desc group_desc(int n, int cin, int h, int w, int cout, int k, int group, int R, Pooling pool,
-                          int pool_group, int convention, b200::Precision prec) {
+                          int pool_group, int convention, b200::Precision prec, int activation = RC_ACT_NONE) {
   rc_desc d{};
   d.n = n;
   d.c_in = cin;
@@ -77,6 +77,7 @@ inline rc_desc group_desc(int n, int cin, int h, int w, int cout, int k, int gro
   d.pool_group = pool_group;
   d.convention = convention;
   d.precision = static_cast<int>(prec);
+  d.activation = activation;
   return d;
 }
 
@@ -345,6 +346,7 @@ struct RILayerSpec {
   int pool_group = 4;
   int convention = RC_CONV_SCATTER;
   b200::Precision precision = b200::Precision::fp32;
+  int activation = RC_ACT_NONE;  // RC_ACT_RELU fuses a ReLU after the bias
 
   int out_orientations() const {
     if (pool == Pooling::none) return orientations;
@@ -365,7 +367,7 @@ inline void ri_conv_forward(const RILayerSpec& s, int n, int cin, int h, int w, 
                             const float* w0, const float* w1, const float* bias, float* y, std::uint8_t* argmax,
                             std::span<const int> devices = {}) {
   const rc_desc d = detail::group_desc(n, cin, h, w, cout, k, s.group, s.orientations, s.pool, s.pool_group,
-                                       s.convention, s.precision);
+                                       s.convention, s.precision, s.activation);
   if (devices.size() > 1)
     b200::throw_on(rc_mgpu_forward_host(&d, x, w0, w1, bias, y, argmax, static_cast<int>(devices.size()),
                                         devices.data()));

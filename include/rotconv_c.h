@@ -36,7 +36,7 @@
 extern "C" {
 #endif
 
-#define RC_ABI_VERSION 1
+#define RC_ABI_VERSION 2
 
 enum rc_status {
   RC_OK = 0,
@@ -59,6 +59,9 @@ enum rc_convention { RC_CONV_SCATTER = 0, RC_CONV_RAW = 1 };
  *   BF16     -- tcgen05 tensor cores, one bf16 product, FP32 accumulate
  *   AUTO     -- fastest kernel that meets the FP32 tolerance for the shape */
 enum rc_precision { RC_PREC_AUTO = 0, RC_PREC_FP32 = 1, RC_PREC_BF16X3 = 2, RC_PREC_BF16 = 3 };
+/* activation fused after the bias (the last op of the epilogue; not in the reference --
+ * used by the multi-layer stack) */
+enum rc_activation { RC_ACT_NONE = 0, RC_ACT_RELU = 1 };
 
 typedef struct rc_desc {
   int n;            /* images in the batch (>= 0) */
@@ -70,6 +73,7 @@ typedef struct rc_desc {
   int pool_group;   /* subgroup_pool_max group_size */
   int convention;   /* rc_convention */
   int precision;    /* rc_precision */
+  int activation;   /* rc_activation (ABI 2) */
 } rc_desc;
 
 /* ---- introspection ------------------------------------------------------ */

@@ -16,12 +16,13 @@ GROUPS = {"single": 0, "p4": 1, "p4m": 2, "steer": 3}
 POOLS = {"none": 0, "avg": 1, "max": 2, "subgroup": 3}
 CONVENTIONS = {"scatter": 0, "raw": 1}
 PRECISIONS = {"auto": 0, "fp32": 1, "bf16x3": 2, "bf16": 3}
+ACTIVATIONS = {"none": 0, "relu": 1}
 
 
 class rc_desc(C.Structure):
     _fields_ = [(n, C.c_int) for n in (
         "n", "c_in", "h", "w", "c_out", "k", "group", "orientations", "pool", "pool_group",
-        "convention", "precision")]
+        "convention", "precision", "activation")]
 
 
 # (name, restype, argtypes) for every symbol include/rotconv_c.h declares

@@ -67,6 +67,8 @@ int validate(const rc_desc& d) {
     return fail(RC_ERR_INVALID, "ri_conv: unknown convention");
   if (d.precision < RC_PREC_AUTO || d.precision > RC_PREC_BF16)
     return fail(RC_ERR_INVALID, "ri_conv: unknown precision");
+  if (d.activation != RC_ACT_NONE && d.activation != RC_ACT_RELU)
+    return fail(RC_ERR_INVALID, "ri_conv: unknown activation");
   return RC_OK;
 }
 
@@ -474,7 +476,7 @@ int rc_tiled_scatter_conv_host(const float* h_x, int c_in, int h, int w, const f
   if (tile_h < 1 || tile_w < 1) return fail(RC_ERR_INVALID, "tiled_scatter_conv: tile dims must be >= 1");
   if (halo != kh / 2) return fail(RC_ERR_INVALID, "tiled_scatter_conv: invalid halo");
   if (workers < 1) return fail(RC_ERR_INVALID, "tiled_scatter_conv: workers must be >= 1");
-  rc_desc d{1, c_in, h, w, c_out, kh, RC_GROUP_SINGLE, 1, RC_POOL_NONE, 1, RC_CONV_SCATTER, RC_PREC_FP32};
+  rc_desc d{1, c_in, h, w, c_out, kh, RC_GROUP_SINGLE, 1, RC_POOL_NONE, 1, RC_CONV_SCATTER, RC_PREC_FP32, RC_ACT_NONE};
   int st = rc_ri_conv_forward_host(&d, h_x, h_wt, nullptr, nullptr, h_y, nullptr, device);
   if (st != RC_OK) return st;
   if (mults) *mults = (unsigned long long)h * w * kh * kw * c_in * c_out;  // :361-366

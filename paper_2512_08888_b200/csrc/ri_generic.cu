@@ -22,7 +22,7 @@ __device__ __forceinline__ void fold(int pool, int k, float v, float& best, int&
 __global__ void generic_kernel(const float* __restrict__ x, const float* __restrict__ bases,
                                const float* __restrict__ bias, float* __restrict__ y,
                                uint8_t* __restrict__ am, int N, int Cin, int H, int W, int Cout,
-                               int K, int NB, int RPB, int pool, int gf, int RO, TapOffsets T) {
+                               int K, int NB, int RPB, int pool, int gf, int RO, int act, TapOffsets T) {
   const long long plane = (long long)H * W;
   const long long total = (long long)N * Cout * plane;
   const int KK = K * K;
@@ -53,7 +53,8 @@ __global__ void generic_kernel(const float* __restrict__ x, const float* __restr
       if (k == gf - 1) {
         float outv = pool == RC_POOL_AVG ? best / (float)R : best;
         const size_t off = (((size_t)n * Cout + co) * RO + slot) * plane + pix;
-        y[off] = outv + bz;
+        const float v = outv + bz;
+        y[off] = act == RC_ACT_RELU ? fmaxf(v, 0.f) : v;
         if (am && (pool == RC_POOL_MAX || pool == RC_POOL_SUBGROUP)) am[off] = (uint8_t)arg;
       }
     }
@@ -101,7 +102,7 @@ int launch_generic(const rc_desc& d, const float* x, const void* bank, const flo
   generic_kernel<<<grid_for(total, 256), 256, 0, s>>>(
       x, reinterpret_cast<const float*>(static_cast<const char*>(bank) + L.bases_off), bias, y,
       has_arg ? argmax : nullptr, d.n, d.c_in, d.h, d.w, d.c_out, d.k, num_bases(d),
-      rot_per_base(d), d.pool, pool_fold(d), out_orientations(d), T);
+      rot_per_base(d), d.pool, pool_fold(d), out_orientations(d), d.activation, T);
   RC_CUDA(cudaGetLastError());
   return RC_OK;
 }

@@ -48,6 +48,7 @@ struct Params {
   float* y;           // [N][Cout][RO][H][W]
   uint8_t* am;        // [N][Cout][RO][H][W] or null
   int N, Cin, H, Cout, NB, pool, gf, RO, COB, IMG;
+  int act;  // rc_activation, applied after the bias
 };
 
 template <int SW, int S, int RPB, int CONV>
@@ -149,6 +150,8 @@ struct SimtK3 {
       *reinterpret_cast<uint32_t*>(dst) = w[0];
   }
 
+  __device__ __forceinline__ float activate(float v) const { return p.act == RC_ACT_RELU ? fmaxf(v, 0.f) : v; }
+
   // pool + bias + store of one finished output row (slot), base b
   template <int SLOT>
   __device__ void finalize(int b, int row) {
@@ -162,7 +165,7 @@ struct SimtK3 {
       for (int r = 0; r < RPB; ++r) {
         float v[SW];
 #pragma unroll
-        for (int j = 0; j < SW; ++j) v[j] = Y[SLOT][r][j] + bz;
+        for (int j = 0; j < SW; ++j) v[j] = activate(Y[SLOT][r][j] + bz);
         store_vec(p.y + ybase + (size_t)(b * RPB + r) * plane, v);
       }
       return;
@@ -182,7 +185,7 @@ struct SimtK3 {
         for (int j = 0; j < SW; ++j) acc[j] += Y[SLOT][r][j];
       if (b == p.NB - 1) {
 #pragma unroll
-        for (int j = 0; j < SW; ++j) acc[j] = acc[j] / (float)R + bz;
+        for (int j = 0; j < SW; ++j) acc[j] = activate(acc[j] / (float)R + bz);
       }
       store_vec(p.y + ybase, acc);
       return;
@@ -221,7 +224,7 @@ struct SimtK3 {
         float v[SW];
         const bool final_ = kk == gf - 1;
 #pragma unroll
-        for (int j = 0; j < SW; ++j) v[j] = final_ ? best[j] + bz : best[j];
+        for (int j = 0; j < SW; ++j) v[j] = final_ ? activate(best[j] + bz) : best[j];
         store_vec(p.y + off, v);
         if (p.am) store_arg(p.am + off, arg);
       }
@@ -382,6 +385,7 @@ int launch_simt_k3(const rc_desc& d, const float* x, const void* bank, const flo
   p.RO = out_orientations(d);
   p.COB = COB;
   p.IMG = IMG;
+  p.act = d.activation;
   const size_t smem = 2 * sizeof(float) * ((size_t)IMG * CC * d.w + (size_t)CC * COB * 12);
   const int gx = (d.c_out + COB - 1) / COB, gy = (d.n + IMG - 1) / IMG;
   if (gy > 65535) return RC_ERR_UNSUPPORTED;

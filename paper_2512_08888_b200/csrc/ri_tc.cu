@@ -71,6 +71,7 @@ struct TcParams {
   uint8_t* am;
   int N, H, Cout, NB, NBK, NC, NCT, pool, gf, RO, passes, w_stages, spc, x_bufs, items;
   float inv_r;  // 1/R for average pooling (R a power of two)
+  int act;      // rc_activation applied after the bias (last op of the epilogue)
   int ablate;   // profiling only: 1 = skip stores, 2 = skip MMAs, 3 = skip MMAs + W loads,
                 // 4 = skip W loads (MMAs on stale tiles), 5 = epilogue skips TMEM loads + scatter
 };
@@ -115,6 +116,10 @@ __device__ __forceinline__ void store_row(const TcParams& p, size_t off, float (
   if (fin) {
 #pragma unroll
     for (int j = 0; j < XH; ++j) v[j] += bz;
+    if (p.act == RC_ACT_RELU) {
+#pragma unroll
+      for (int j = 0; j < XH; ++j) v[j] = fmaxf(v[j], 0.f);
+    }
   }
   store8(p.y + off, v);
   if (p.am) *reinterpret_cast<uint4*>(p.am + off) = make_uint4(arg[0], arg[1], arg[2], arg[3]);
@@ -123,12 +128,17 @@ __device__ __forceinline__ void store_row(const TcParams& p, size_t off, float (
 // pool + bias + store one output row (16 px) of base b; same semantics as ri_simt.cu.
 // Fold groups gf in {1, 2, 4} stay inside a base; gf % 4 == 0 spans bases through a
 // partial (value, argmax) kept in the output row itself (same thread, program order).
-template <int TW>
-__device__ __forceinline__ void finalize_row(const TcParams& p, float (&Yr)[4][XH], int n, int co, int b,
+template <int TW, int RPB>
+__device__ __forceinline__ void finalize_row(const TcParams& p, float (&Yr)[RPB][XH], int n, int co, int b,
                                              int row, int x0) {
   const size_t plane = (size_t)p.H * TW;
   const size_t ybase = ((size_t)n * p.Cout + co) * p.RO * plane + (size_t)row * TW + x0;
   const float bz = p.bias ? p.bias[co] : 0.f;
+  if constexpr (RPB == 1) {  // single orientation: every reduction of one slice is the slice
+    const uint32_t z[XH / 4] = {0, 0, 0, 0};
+    store_row(p, ybase, Yr[0], z, bz, true);
+    return;
+  } else {
   if (p.pool == RC_POOL_NONE) {
     const uint32_t z[XH / 4] = {0, 0, 0, 0};
 #pragma unroll
@@ -180,6 +190,7 @@ __device__ __forceinline__ void finalize_row(const TcParams& p, float (&Yr)[4][X
     }
     store_row(p, off, Yr[0], arg, bz, kk0 + 4 == gf);
   }
+  }
 }
 
 // ---- scatter ------------------------------------------------------------------------
@@ -188,10 +199,10 @@ __device__ __forceinline__ void finalize_row(const TcParams& p, float (&Yr)[4][X
 // outside the image were loaded as 0 (TW = 32) or are skipped at compile time (TW = 16:
 // the thread's 16 columns are the whole row).  Y_r(p) += Z_t(p + (di, dj)): for tap T and
 // rotation r the single contributing row is I = 1 + di.
-template <int TW, int CONV, int T, int I>
-__device__ __forceinline__ void scatter_row(float (&Y)[4][XH], const float (&z)[18]) {
+template <int TW, int RPB, int CONV, int T, int I>
+__device__ __forceinline__ void scatter_row(float (&Y)[RPB][XH], const float (&z)[18]) {
 #pragma unroll
-  for (int r = 0; r < 4; ++r) {
+  for (int r = 0; r < RPB; ++r) {
     const int di = make_k3(CONV).di[r][T];
     const int dj = make_k3(CONV).dj[r][T];
     if (1 + di != I) continue;
@@ -236,17 +247,17 @@ struct EpiState {
 };
 
 // one tap (compile-time T): three single-row TMEM round trips, D released after the last
-template <int TW, int CONV, int T>
-__device__ __forceinline__ void epi_tap(EpiState& e, float (&Y)[4][XH], uint64_t* d_full, uint64_t* d_empty) {
+template <int TW, int RPB, int CONV, int T>
+__device__ __forceinline__ void epi_tap(EpiState& e, float (&Y)[RPB][XH], uint64_t* d_full, uint64_t* d_empty) {
   constexpr int NDB = Geo<TW>::NDB;
   const uint32_t a = e.row_base + e.db * Geo<TW>::BAND_PX;
   float z[18];
   mbar_wait(&d_full[e.db], e.dph);
   tc_fence_after();
   load_row<TW>(a, e.half, z);
-  scatter_row<TW, CONV, T, 0>(Y, z);
+  scatter_row<TW, RPB, CONV, T, 0>(Y, z);
   load_row<TW>(a + TW, e.half, z);
-  scatter_row<TW, CONV, T, 1>(Y, z);
+  scatter_row<TW, RPB, CONV, T, 1>(Y, z);
   load_row<TW>(a + 2 * TW, e.half, z);
   tc_fence_before();
   __syncwarp();
@@ -255,12 +266,12 @@ __device__ __forceinline__ void epi_tap(EpiState& e, float (&Y)[4][XH], uint64_t
     e.db = 0;
     e.dph ^= 1;
   }
-  scatter_row<TW, CONV, T, 2>(Y, z);
+  scatter_row<TW, RPB, CONV, T, 2>(Y, z);
 }
 
 // Epilogue warp: lane quadrant q (co = q*32 + lane); sub-tile sub = (output row of the
 // band, column half): TW = 16 -> 4 rows x 1 half, TW = 32 -> 2 rows x 2 halves.
-template <int TW, int CONV>
+template <int TW, int RPB, int CONV>
 __device__ void epilogue(const TcParams& p, uint32_t tmem, uint64_t* d_full, uint64_t* d_empty) {
   using G = Geo<TW>;
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
@@ -269,7 +280,7 @@ __device__ void epilogue(const TcParams& p, uint32_t tmem, uint64_t* d_full, uin
   const int srow = sub / G::HALVES, half = sub % G::HALVES;
   const int co_l = q * 32 + lane;
   EpiState e{tmem + ((uint32_t)(q * 32) << 16) + D0 + srow * TW + half * 16, 0, 0, lane, half};
-  float Y[4][XH];
+  float Y[RPB][XH];
   for (int item = blockIdx.x; item < p.items; item += gridDim.x) {
     const int n = item / p.NCT, ct = item % p.NCT;
     const int co = ct * 128 + co_l;
@@ -288,20 +299,20 @@ __device__ void epilogue(const TcParams& p, uint32_t tmem, uint64_t* d_full, uin
     for (int b = 0; b < p.NB; ++b)
       for (int k = 0; k < p.NBK; ++k) {
 #pragma unroll
-        for (int r = 0; r < 4; ++r)
+        for (int r = 0; r < RPB; ++r)
 #pragma unroll
           for (int x = 0; x < XH; ++x) Y[r][x] = 0.f;
-        epi_tap<TW, CONV, 0>(e, Y, d_full, d_empty);
-        epi_tap<TW, CONV, 1>(e, Y, d_full, d_empty);
-        epi_tap<TW, CONV, 2>(e, Y, d_full, d_empty);
-        epi_tap<TW, CONV, 3>(e, Y, d_full, d_empty);
-        epi_tap<TW, CONV, 4>(e, Y, d_full, d_empty);
-        epi_tap<TW, CONV, 5>(e, Y, d_full, d_empty);
-        epi_tap<TW, CONV, 6>(e, Y, d_full, d_empty);
-        epi_tap<TW, CONV, 7>(e, Y, d_full, d_empty);
-        epi_tap<TW, CONV, 8>(e, Y, d_full, d_empty);
+        epi_tap<TW, RPB, CONV, 0>(e, Y, d_full, d_empty);
+        epi_tap<TW, RPB, CONV, 1>(e, Y, d_full, d_empty);
+        epi_tap<TW, RPB, CONV, 2>(e, Y, d_full, d_empty);
+        epi_tap<TW, RPB, CONV, 3>(e, Y, d_full, d_empty);
+        epi_tap<TW, RPB, CONV, 4>(e, Y, d_full, d_empty);
+        epi_tap<TW, RPB, CONV, 5>(e, Y, d_full, d_empty);
+        epi_tap<TW, RPB, CONV, 6>(e, Y, d_full, d_empty);
+        epi_tap<TW, RPB, CONV, 7>(e, Y, d_full, d_empty);
+        epi_tap<TW, RPB, CONV, 8>(e, Y, d_full, d_empty);
         const int row = G::OUT_ROWS * k + srow;
-        if (n < p.N && co < p.Cout && row < p.H && p.ablate != 1) finalize_row<TW>(p, Y, n, co, b, row, half * 16);
+        if (n < p.N && co < p.Cout && row < p.H && p.ablate != 1) finalize_row<TW, RPB>(p, Y, n, co, b, row, half * 16);
       }
   }
 }
@@ -319,7 +330,7 @@ struct Ring {
   }
 };
 
-template <int TW, int CONV>
+template <int TW, int RPB, int CONV>
 __global__ void __launch_bounds__(THREADS, 1) ri_tc_kernel(const __grid_constant__ TcParams p) {
   using G = Geo<TW>;
   constexpr int NDB = G::NDB;
@@ -462,7 +473,7 @@ __global__ void __launch_bounds__(THREADS, 1) ri_tc_kernel(const __grid_constant
   } else if (warp >= EPI_WARP0) {
     // ------------------------------------------------------------ epilogue
     asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(REGS_EPILOGUE));
-    epilogue<TW, CONV>(p, tmem, d_full, d_empty);
+    epilogue<TW, RPB, CONV>(p, tmem, d_full, d_empty);
   }
   tc_fence_before();
   __syncthreads();
@@ -587,14 +598,14 @@ bool tc_supported(const rc_desc& d) {
   const int R = d.orientations;
   const bool fold_ok = d.pool == RC_POOL_NONE || (d.pool == RC_POOL_AVG && (R & (R - 1)) == 0) || gf == 1 ||
                        gf == 2 || gf % 4 == 0;
-  if (!(d.k == 3 && (d.w == 16 || d.w == 32) && d.group != RC_GROUP_SINGLE && fold_ok &&
+  if (!(d.k == 3 && (d.w == 16 || d.w == 32) && fold_ok &&
         (d.precision == RC_PREC_BF16 || d.precision == RC_PREC_BF16X3 || d.precision == RC_PREC_AUTO)))
     return false;
   const int parts = d.precision == RC_PREC_BF16 ? 1 : 2;
   return smem_plan(geom(d), parts).spc > 0;
 }
 size_t tc_bank_bytes(const rc_desc& d) {
-  if (!(d.k == 3 && d.group != RC_GROUP_SINGLE)) return 0;
+  if (d.k != 3) return 0;
   return 3 * geom(d).w_plane;  // interleaved hi/lo + hi-only
 }
 size_t tc_workspace_bytes(const rc_desc& d) {
@@ -655,6 +666,7 @@ int launch_tc(const rc_desc& d, const float* x, const void* bank, const float* b
   p.RO = out_orientations(d);
   p.passes = passes;
   p.inv_r = 1.0f / (float)d.orientations;
+  p.act = d.activation;
   p.w_stages = plan.stages;
   p.spc = plan.spc;
   p.x_bufs = plan.x_bufs;
@@ -667,8 +679,11 @@ int launch_tc(const rc_desc& d, const float* x, const void* bank, const float* b
   RC_CUDA(cudaGetDevice(&dev));
   RC_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
   const int grid = p.items < sms ? p.items : sms;
-  void (*fn)(TcParams) = d.w == 32 ? (d.convention == RC_CONV_RAW ? ri_tc_kernel<32, 1> : ri_tc_kernel<32, 0>)
-                                    : (d.convention == RC_CONV_RAW ? ri_tc_kernel<16, 1> : ri_tc_kernel<16, 0>);
+  // [width][single][convention]
+  static void (*const kernels[2][2][2])(TcParams) = {
+      {{ri_tc_kernel<16, 4, 0>, ri_tc_kernel<16, 4, 1>}, {ri_tc_kernel<16, 1, 0>, ri_tc_kernel<16, 1, 1>}},
+      {{ri_tc_kernel<32, 4, 0>, ri_tc_kernel<32, 4, 1>}, {ri_tc_kernel<32, 1, 0>, ri_tc_kernel<32, 1, 1>}}};
+  void (*fn)(TcParams) = kernels[d.w == 32][d.group == RC_GROUP_SINGLE][d.convention == RC_CONV_RAW];
   RC_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)plan.bytes));
   fn<<<grid, THREADS, plan.bytes, s>>>(p);
   RC_CUDA(cudaGetLastError());

@@ -114,12 +114,13 @@ class Desc:
     pool_group: int = 4
     convention: str = "scatter"
     precision: str = "fp32"
+    activation: str = "none"
 
     def c(self) -> rc_desc:
         return rc_desc(self.n, self.c_in, self.h, self.w, self.c_out, self.k,
                        _lib.GROUPS[self.group], self.orientations, _lib.POOLS[self.pool],
                        self.pool_group, _lib.CONVENTIONS[self.convention],
-                       _lib.PRECISIONS[self.precision])
+                       _lib.PRECISIONS[self.precision], _lib.ACTIVATIONS[self.activation])
 
     def validate(self) -> None:
         d = self.c()

@@ -31,7 +31,7 @@ def test_library_exports_every_declared_symbol():
     for s in declared_symbols():
         assert hasattr(L, s), s
         assert s in _lib.SIGNATURES, f"{s} has no ctypes signature"
-    assert L.rc_abi_version() == 1
+    assert L.rc_abi_version() == 2
 
 
 def test_validation_messages_match_reference():

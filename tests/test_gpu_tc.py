@@ -139,6 +139,47 @@ def test_tc_w32_c4_shape_random(O, dev, precision):
     assert err <= TOL[precision], f"normwise {err:.3e}"
 
 
+@pytest.mark.parametrize("precision", ["bf16", "bf16x3"])
+@pytest.mark.parametrize("cfg", [(2, 64, 16, 16, 256, "scatter", "none"), (3, 32, 9, 16, 130, "raw", "max"),
+                                 (2, 128, 32, 32, 128, "scatter", "avg"), (1, 16, 5, 32, 64, "raw", "none")],
+                         ids=lambda c: "-".join(map(str, c)))
+def test_tc_single_orientation_dyadic(O, dev, cfg, precision):
+    """R = 1 (tiled_scatter_conv semantics) on the tensor cores, bit-exact on dyadic inputs."""
+    import paper_2512_08888_b200 as P
+    n, cin, h, w, cout, conv, pool = cfg
+    d = O.Desc(n, cin, h, w, cout, 3, "single", 1, pool, 1, conv)
+    rng = np.random.default_rng(abs(hash(cfg)) % 2**32)
+    x = dyadic(rng, (n, cin, h, w))
+    w0 = dyadic(rng, (cout, cin, 3, 3))
+    bias = dyadic(rng, cout)
+    y_ref, a_ref = O.ri_forward(d, x, w0, None, bias)
+    y, a = run(P, d, x, w0, None, bias, precision, dev)
+    assert np.array_equal(y.reshape(y_ref.shape), y_ref), f"max|dy| = {np.abs(y.reshape(y_ref.shape) - y_ref).max()}"
+    if a_ref is not None:
+        assert not a.any()
+
+
+@pytest.mark.parametrize("kernel", ["tc", "simt"])
+def test_fused_relu_activation(O, dev, kernel):
+    """activation = relu is applied after the bias (relu of the oracle's pooled output)."""
+    import paper_2512_08888_b200 as P
+    n, cin, h, cout = 2, 64, 16, 128
+    rng = np.random.default_rng(5)
+    x = dyadic(rng, (n, cin, h, 16))
+    w0 = dyadic(rng, (cout, cin, 3, 3))
+    bias = dyadic(rng, cout)
+    d = O.Desc(n, cin, h, 16, cout, 3, "p4m", 8, "subgroup", 4)
+    y_ref, a_ref = O.ri_forward(d, x, w0, None, bias)
+    t = lambda a: torch.from_numpy(a).to(dev)
+    desc = P.Desc(n, cin, h, 16, cout, 3, "p4m", 8, "subgroup", 4, "scatter",
+                  "bf16x3" if kernel == "tc" else "fp32", "relu")
+    assert desc.kernel_name().startswith("tc_" if kernel == "tc" else "simt")
+    bank = P.bank_precompute(desc, t(w0))
+    y, a = P.ri_conv_forward(desc, t(x), bank, t(bias))
+    assert np.array_equal(y.cpu().numpy(), np.maximum(y_ref, 0))
+    assert np.array_equal(a.cpu().numpy(), a_ref)
+
+
 def test_tc_matches_simt_on_c3_shape_subset(O, dev):
     """C3 layer shape (256 -> 1024, steer R=8, subgroup-4) on 8 images: bf16x3 vs the
     FP32 CUDA-core kernel, normwise, plus determinism."""
