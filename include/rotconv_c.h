@@ -78,6 +78,12 @@ typedef struct rc_desc {
 
 /* ---- introspection ------------------------------------------------------ */
 int rc_abi_version(void);
+/* Main-kernel timing for benchmarks/profilers: while enabled on the calling thread, every
+ * conv launch brackets its main kernel (not operand packing) with a CUDA event pair on its
+ * stream; rc_profile_collect synchronises and returns the durations (ms) in launch order.
+ * Enabling again clears the list. */
+int rc_profile_enable(int on);
+int rc_profile_collect(float* ms, int max_n);
 const char* rc_last_error(void);
 /* RC_OK or RC_ERR_INVALID (message via rc_last_error) */
 int rc_validate(const rc_desc* d);
@@ -130,6 +136,14 @@ const char* rc_kernel_name(const rc_desc* d);
 int rc_orientation_pool(int n, int c_out, int r, int h, int w, int pool, int pool_group,
                         const float* d_f, const float* d_bias, float* d_y, uint8_t* d_argmax,
                         void* stream);
+
+/* ---- multi-layer stack glue (config C5; not in the reference) -----
+ * 2x2 max pooling of an NCHW batch (H even, W a multiple of 4) and the classifier head:
+ * global average pooling over H*W followed by logits = feat @ Wc^T + bc
+ * (Wc: classes x C row-major, bc nullable). */
+int rc_maxpool2x2(int n, int c, int h, int w, const float* d_x, float* d_y, void* stream);
+int rc_gap_linear(int n, int c, int h, int w, const float* d_x, const float* d_wc, const float* d_bc,
+                  int classes, float* d_out, void* stream);
 
 /* ---- host-buffer drop-in entry points ------------------------------------
  * The whole layer with host (ideally pinned) buffers on device `device`:

@@ -31,6 +31,8 @@ _D = _P(rc_desc)
 _VP = C.c_void_p
 SIGNATURES = {
     "rc_abi_version": (C.c_int, []),
+    "rc_profile_enable": (C.c_int, [C.c_int]),
+    "rc_profile_collect": (C.c_int, [_P(C.c_float), C.c_int]),
     "rc_last_error": (C.c_char_p, []),
     "rc_validate": (C.c_int, [_D]),
     "rc_num_bases": (C.c_int, [_D]),
@@ -51,6 +53,8 @@ SIGNATURES = {
     "rc_orientation_bank_host": (C.c_int, [_D, _VP, _VP, _VP, C.c_int]),
     "rc_orientation_pool_host": (C.c_int, [C.c_int] * 7 + [_VP, _VP, _VP, _VP, C.c_int]),
     "rc_mgpu_forward_host": (C.c_int, [_D, _VP, _VP, _VP, _VP, _VP, _VP, C.c_int, _P(C.c_int)]),
+    "rc_maxpool2x2": (C.c_int, [C.c_int] * 4 + [_VP, _VP, _VP]),
+    "rc_gap_linear": (C.c_int, [C.c_int] * 4 + [_VP, _VP, _VP, C.c_int, _VP, _VP]),
     "rc_tiled_scatter_conv_host": (C.c_int, [_VP] + [C.c_int] * 3 + [_VP] + [C.c_int] * 9 +
                                    [_VP, _P(C.c_ulonglong), _P(C.c_ulonglong),
                                     _P(C.c_ulonglong), C.c_int]),

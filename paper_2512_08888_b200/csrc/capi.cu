@@ -15,10 +15,30 @@ namespace rc {
 
 namespace {
 thread_local std::string g_err;
+struct ProfState {
+  bool on = false;
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> pairs;
+  size_t used = 0;
+};
+thread_local ProfState g_prof;
 size_t align256(size_t v) { return (v + 255) & ~size_t(255); }
 }  // namespace
 
 void set_error(const std::string& msg) { g_err = msg; }
+
+void prof_begin(cudaStream_t s) {
+  if (!g_prof.on) return;
+  if (g_prof.used == g_prof.pairs.size()) {
+    cudaEvent_t a, b;
+    if (cudaEventCreate(&a) != cudaSuccess || cudaEventCreate(&b) != cudaSuccess) return;
+    g_prof.pairs.emplace_back(a, b);
+  }
+  cudaEventRecord(g_prof.pairs[g_prof.used].first, s);
+}
+void prof_end(cudaStream_t s) {
+  if (!g_prof.on || g_prof.used == g_prof.pairs.size()) return;
+  cudaEventRecord(g_prof.pairs[g_prof.used++].second, s);
+}
 int fail(int status, const std::string& msg) {
   g_err = msg;
   return status;
@@ -124,6 +144,18 @@ namespace {
 struct DeviceCache {
   std::mutex mu;
   cudaStream_t stream = nullptr;
+  cudaStream_t h2d = nullptr, d2h = nullptr;  // copy engines of the chunked host pipeline
+  std::vector<cudaEvent_t> ev;                 // pipeline events (grow-only)
+  int ensure_pipeline(size_t events) {
+    if (!h2d) RC_CUDA(cudaStreamCreateWithFlags(&h2d, cudaStreamNonBlocking));
+    if (!d2h) RC_CUDA(cudaStreamCreateWithFlags(&d2h, cudaStreamNonBlocking));
+    while (ev.size() < events) {
+      cudaEvent_t e;
+      RC_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+      ev.push_back(e);
+    }
+    return RC_OK;
+  }
   std::vector<std::pair<void*, size_t>> bufs;  // grow-only slots
   void* get(int slot, size_t bytes) {
     if ((int)bufs.size() <= slot) bufs.resize(slot + 1, {nullptr, 0});
@@ -157,11 +189,14 @@ struct DeviceGuard {
 // (never silently a different arithmetic); AUTO -> tensor cores where supported.
 int dispatch(const rc_desc& d, const float* x, const void* bank, const float* bias, float* y,
              uint8_t* am, void* ws, size_t ws_bytes, cudaStream_t s, bool dry, const char** name) {
-  if (d.precision == RC_PREC_BF16X3 || d.precision == RC_PREC_BF16 || d.precision == RC_PREC_AUTO) {
+  // AUTO keeps tiny channel counts on the CUDA cores: the tensor-core K chunk is 64 input
+  // channels, so Cin < 16 would multiply mostly zero padding (e.g. an RGB first layer).
+  const bool auto_tc = d.precision == RC_PREC_AUTO && d.c_in >= 16;
+  if (d.precision == RC_PREC_BF16X3 || d.precision == RC_PREC_BF16 || auto_tc) {
     int st = launch_tc(d, x, bank, bias, y, am, ws, ws_bytes, s, dry, name);
     if (st != RC_ERR_UNSUPPORTED || d.precision != RC_PREC_AUTO) {
       if (st == RC_ERR_UNSUPPORTED)
-        return fail(st, "ri_conv: no tensor-core kernel for this shape (K=3, W=16, rotation group)");
+        return fail(st, "ri_conv: no tensor-core kernel for this shape (needs K=3 and W = 16, 32 or a multiple of 16 >= 48)");
       return st;
     }
   }
@@ -182,6 +217,21 @@ int dispatch(const rc_desc& d, const float* x, const void* bank, const float* bi
 extern "C" {
 
 int rc_abi_version(void) { return RC_ABI_VERSION; }
+
+int rc_profile_enable(int on) {
+  g_prof.on = on != 0;
+  if (g_prof.on) g_prof.used = 0;
+  return RC_OK;
+}
+
+int rc_profile_collect(float* ms, int max_n) {
+  int n = 0;
+  for (size_t i = 0; i < g_prof.used && n < max_n; ++i, ++n) {
+    RC_CUDA(cudaEventSynchronize(g_prof.pairs[i].second));
+    RC_CUDA(cudaEventElapsedTime(&ms[n], g_prof.pairs[i].first, g_prof.pairs[i].second));
+  }
+  return n;
+}
 const char* rc_last_error(void) { return g_err.c_str(); }
 
 int rc_validate(const rc_desc* d) {
@@ -313,17 +363,39 @@ int rc_ri_conv_forward_host(const rc_desc* d, const float* h_x, const float* h_w
       (h_bias && !dbias) || (has_arg && !da) || (wsb && !dws))
     return fail(RC_ERR_CUDA, "ri_conv: device allocation failed");
   cudaStream_t s = c.stream;
-  RC_CUDA(cudaMemcpyAsync(dx, h_x, xb, cudaMemcpyHostToDevice, s));
   RC_CUDA(cudaMemcpyAsync(dw0, h_w0, wb, cudaMemcpyHostToDevice, s));
   if (dw1) RC_CUDA(cudaMemcpyAsync(dw1, h_w1, wb, cudaMemcpyHostToDevice, s));
   if (dbias) RC_CUDA(cudaMemcpyAsync(dbias, h_bias, d->c_out * sizeof(float), cudaMemcpyHostToDevice, s));
   int st = launch_bank(*d, (const float*)dw0, (const float*)dw1, dbank, s);
   if (st != RC_OK) return st;
-  st = dispatch(*d, (const float*)dx, dbank, (const float*)dbias, (float*)dy, (uint8_t*)da, dws, wsb, s,
-                false, nullptr);
+  // Chunked pipeline over images: H2D of chunk i+1 and D2H of chunk i-1 overlap the kernels
+  // of chunk i (three streams, the copies on the two copy engines).  Chunks of >= 16 images
+  // keep every copy large; small batches run as one chunk.
+  const int chunks = d->n >= 64 ? 8 : (d->n >= 32 ? 4 : 1);
+  st = c.ensure_pipeline(2 * (size_t)chunks);
   if (st != RC_OK) return st;
-  RC_CUDA(cudaMemcpyAsync(h_y, dy, yb, cudaMemcpyDeviceToHost, s));
-  if (has_arg) RC_CUDA(cudaMemcpyAsync(h_argmax, da, ab, cudaMemcpyDeviceToHost, s));
+  const size_t xi = xb / d->n, yi = yb / d->n, ai = ab / d->n;
+  for (int k = 0; k < chunks; ++k) {
+    int b = 0, e = 0;
+    rc_shard_range(d->n, chunks, k, &b, &e);
+    if (e == b) continue;
+    cudaEvent_t in_ready = c.ev[2 * k], out_ready = c.ev[2 * k + 1];
+    RC_CUDA(cudaMemcpyAsync((char*)dx + b * xi, (const char*)h_x + b * xi, (e - b) * xi, cudaMemcpyHostToDevice,
+                            c.h2d));
+    RC_CUDA(cudaEventRecord(in_ready, c.h2d));
+    RC_CUDA(cudaStreamWaitEvent(s, in_ready, 0));
+    rc_desc cd = *d;
+    cd.n = e - b;
+    st = dispatch(cd, (const float*)((char*)dx + b * xi), dbank, (const float*)dbias, (float*)((char*)dy + b * yi),
+                  da ? (uint8_t*)da + b * ai : nullptr, dws, wsb, s, false, nullptr);
+    if (st != RC_OK) return st;
+    RC_CUDA(cudaEventRecord(out_ready, s));
+    RC_CUDA(cudaStreamWaitEvent(c.d2h, out_ready, 0));
+    RC_CUDA(cudaMemcpyAsync((char*)h_y + b * yi, (char*)dy + b * yi, (e - b) * yi, cudaMemcpyDeviceToHost, c.d2h));
+    if (has_arg)
+      RC_CUDA(cudaMemcpyAsync(h_argmax + b * ai, (uint8_t*)da + b * ai, (e - b) * ai, cudaMemcpyDeviceToHost, c.d2h));
+  }
+  RC_CUDA(cudaStreamSynchronize(c.d2h));
   RC_CUDA(cudaStreamSynchronize(s));
   return RC_OK;
 }

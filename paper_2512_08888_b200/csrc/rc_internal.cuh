@@ -40,6 +40,12 @@ inline int pool_fold(const rc_desc& d) {
 }
 int validate(const rc_desc& d);  // RC_OK or RC_ERR_INVALID + message
 
+// ---- main-kernel timing (rc_profile_enable / rc_profile_collect) -------------------------
+// When enabled on the calling thread, every conv launch brackets its MAIN kernel (not the
+// operand packing) with a CUDA event pair on the launch stream.
+void prof_begin(cudaStream_t s);
+void prof_end(cudaStream_t s);
+
 // ---- bank layout (rc_bank_bytes) ---------------------------------------------------
 struct BankLayout {
   size_t bases_off, bases_bytes;  // fp32 [B][Cout][Cin][K][K]
@@ -71,6 +77,10 @@ int launch_generic(const rc_desc& d, const float* x, const void* bank, const flo
                    float* y, uint8_t* argmax, cudaStream_t s, const char** name);
 int launch_pool(int n, int c_out, int r, int h, int w, int pool, int g, const float* f,
                 const float* bias, float* y, uint8_t* argmax, cudaStream_t s);
+// stack glue (stack.cu)
+int launch_maxpool2x2(int n, int c, int h, int w, const float* x, float* y, cudaStream_t s);
+int launch_gap_linear(int n, int c, int h, int w, const float* x, const float* wc, const float* bc, int classes,
+                      float* out, cudaStream_t s);
 
 }  // namespace rc
 

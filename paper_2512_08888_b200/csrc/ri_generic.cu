@@ -99,10 +99,12 @@ int launch_generic(const rc_desc& d, const float* x, const void* bank, const flo
   slice_tap_offsets(d.k, d.convention, &T);
   const BankLayout L = bank_layout(d);
   const bool has_arg = d.pool == RC_POOL_MAX || d.pool == RC_POOL_SUBGROUP;
+  prof_begin(s);
   generic_kernel<<<grid_for(total, 256), 256, 0, s>>>(
       x, reinterpret_cast<const float*>(static_cast<const char*>(bank) + L.bases_off), bias, y,
       has_arg ? argmax : nullptr, d.n, d.c_in, d.h, d.w, d.c_out, d.k, num_bases(d),
       rot_per_base(d), d.pool, pool_fold(d), out_orientations(d), d.activation, T);
+  prof_end(s);
   RC_CUDA(cudaGetLastError());
   return RC_OK;
 }

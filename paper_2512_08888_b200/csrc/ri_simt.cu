@@ -109,11 +109,13 @@ struct SimtK3 {
     cp_async_commit();
   }
 
-  __device__ __forceinline__ void compute_stage(const float* st) {
+  // ncl = channels of this chunk (CC, fewer for the last chunk of a small / ragged Cin:
+  // the zero-filled tail channels are skipped instead of multiplied)
+  __device__ __forceinline__ void compute_stage(const float* st, int ncl) {
     const float* sx = st + img_l * CC * W + x0;
     const float4* sw = reinterpret_cast<const float4*>(st + stage_x) + co_l * 3;
 #pragma unroll 4
-    for (int cl = 0; cl < CC; ++cl) {
+    for (int cl = 0; cl < ncl; ++cl) {
       float xv[SW];
 #pragma unroll
       for (int v = 0; v < SW / 4; ++v) {
@@ -255,7 +257,7 @@ struct SimtK3 {
         issue(gi + 1, total);
         cp_async_wait<1>();
         __syncthreads();
-        compute_stage(smem + (gi & 1) * stage_floats);
+        compute_stage(smem + (gi & 1) * stage_floats, min(CC, p.Cin - c * CC));
         __syncthreads();
       }
     }
@@ -321,7 +323,9 @@ template <int SW, int S, int RPB, int CONV>
 int launch_t(const Params& p, int grid_x, int grid_y, int threads, size_t smem, cudaStream_t s) {
   auto fn = simt_k3_kernel<SW, S, RPB, CONV>;
   RC_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  prof_begin(s);
   fn<<<dim3(grid_x, grid_y), threads, smem, s>>>(p);
+  prof_end(s);
   RC_CUDA(cudaGetLastError());
   return RC_OK;
 }

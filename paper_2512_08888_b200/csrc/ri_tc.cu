@@ -38,17 +38,24 @@ namespace {
 
 using namespace tc;
 
-// Band geometry per image width TW (16 or 32): a band is OUT_ROWS output rows (64 output
-// pixels, the register budget of the epilogue) computed from IN_ROWS = OUT_ROWS + 2 input
-// rows; every epilogue thread owns 16 pixels (one row of TW = 16, half a row of TW = 32).
+// Band geometry.  A band is 64 output pixels (the register budget of the epilogue: every
+// epilogue thread owns 16 of them) computed from the input rows/columns they depend on:
+//   TW = 16 : 4 full rows of a 16-wide image from 6 input rows           (N = 96)
+//   TW = 32 : 2 full rows of a 32-wide image from 4 input rows           (N = 128)
+//   TW = 0  : strip of 4 rows x 16 columns of a wider image (W % 16 == 0, W >= 48) from
+//             6 input rows x 18 columns incl. the halo columns           (N = 112, 108 used)
+// RS is the TMEM / operand row stride (pixels per input row of the band).
 template <int TW>
 struct Geo {
-  static constexpr int OUT_ROWS = 64 / TW;               // 4 | 2
-  static constexpr int IN_ROWS = OUT_ROWS + 2;           // 6 | 4
-  static constexpr int BAND_PX = IN_ROWS * TW;           // 96 | 128 = N of the MMA
-  static constexpr int XTILE = BAND_PX * 64 * 2;         // bytes of one [BAND_PX x 64 ci] bf16 tile
-  static constexpr int HALVES = TW / 16;                 // epilogue threads per output row
-  static constexpr int NDB = TW == 16 ? 4 : 3;           // TMEM D buffers: 16 + NDB*BAND_PX <= 512
+  static constexpr bool STRIP = TW == 0;
+  static constexpr int OUT_ROWS = STRIP ? 4 : 64 / TW;      // 4 | 2 | 4
+  static constexpr int IN_ROWS = OUT_ROWS + 2;              // 6 | 4 | 6
+  static constexpr int RS = STRIP ? 18 : TW;                // 16 | 32 | 18
+  static constexpr int BAND_PX = IN_ROWS * RS;              // 96 | 128 | 108
+  static constexpr int MMA_N = (BAND_PX + 15) / 16 * 16;    // 96 | 128 | 112
+  static constexpr int XTILE = MMA_N * 64 * 2;              // bytes of one [MMA_N x 64 ci] bf16 tile
+  static constexpr int HALVES = STRIP ? 1 : TW / 16;        // epilogue threads per output row
+  static constexpr int NDB = MMA_N * 4 + 16 <= 512 ? 4 : 3; // TMEM D buffers
 };
 constexpr int KC = 64;                  // ci per chunk (one 128-byte swizzle row of bf16)
 constexpr int WTILE = 128 * KC * 2;      // 16 KB
@@ -58,6 +65,7 @@ constexpr int THREADS = 32 * (EPI_WARP0 + NUM_EPI);
 constexpr int REGS_PRODUCER = 32;        // setmaxnreg budgets: 20 warps x 96 at launch
 constexpr int REGS_EPILOGUE = 112;
 constexpr int MAX_NDB = 4;
+constexpr int MAX_NC = 8;                // ci chunks of 64 (Cin <= 512)
 constexpr uint32_t D0 = 16;              // D buffers from column 16: the 1-column-left halo
                                          // load of a band's first pixel stays in the allocation
 constexpr int XH = 16;                   // output columns per epilogue thread
@@ -69,7 +77,8 @@ struct TcParams {
   const float* bias;
   float* y;
   uint8_t* am;
-  int N, H, Cout, NB, NBK, NC, NCT, pool, gf, RO, passes, w_stages, spc, x_bufs, items;
+  int N, H, W, Cout, NB, NBK, NC, NCT, pool, gf, RO, passes, w_stages, spc, items;
+  int xstream;  // 1: X chunks travel with the W stages (the X band does not fit in smem)
   float inv_r;  // 1/R for average pooling (R a power of two)
   int act;      // rc_activation applied after the bias (last op of the epilogue)
   int ablate;   // profiling only: 1 = skip stores, 2 = skip MMAs, 3 = skip MMAs + W loads,
@@ -131,8 +140,9 @@ __device__ __forceinline__ void store_row(const TcParams& p, size_t off, float (
 template <int TW, int RPB>
 __device__ __forceinline__ void finalize_row(const TcParams& p, float (&Yr)[RPB][XH], int n, int co, int b,
                                              int row, int x0) {
-  const size_t plane = (size_t)p.H * TW;
-  const size_t ybase = ((size_t)n * p.Cout + co) * p.RO * plane + (size_t)row * TW + x0;
+  const int wimg = TW ? TW : p.W;
+  const size_t plane = (size_t)p.H * wimg;
+  const size_t ybase = ((size_t)n * p.Cout + co) * p.RO * plane + (size_t)row * wimg + x0;
   const float bz = p.bias ? p.bias[co] : 0.f;
   if constexpr (RPB == 1) {  // single orientation: every reduction of one slice is the slice
     const uint32_t z[XH / 4] = {0, 0, 0, 0};
@@ -222,9 +232,24 @@ __device__ __forceinline__ float tmem_ld1(uint32_t taddr) {
 }
 
 // one input row of the thread's window: 16 columns + (TW = 32) the two halo columns
+__device__ __forceinline__ void tmem_ld2f(uint32_t taddr, float& a, float& b) {
+  uint32_t r0, r1;
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x2.b32 {%0,%1}, [%2];\n" : "=r"(r0), "=r"(r1) : "r"(taddr));
+  a = __uint_as_float(r0);
+  b = __uint_as_float(r1);
+}
+
 template <int TW>
 __device__ __forceinline__ void load_row(uint32_t a, int half, float (&z)[18]) {
   float v[16];
+  if constexpr (TW == 0) {  // strip: the band row holds the halo columns (zero at image edges)
+    tmem_ld16(a, v);
+    tmem_ld2f(a + 16, z[16], z[17]);
+    tmem_wait_ld();
+#pragma unroll
+    for (int i = 0; i < 16; ++i) z[i] = v[i];
+    return;
+  }
   tmem_ld16(a, v);
   if (TW == 32) {
     z[0] = tmem_ld1(a - 1);
@@ -250,15 +275,15 @@ struct EpiState {
 template <int TW, int RPB, int CONV, int T>
 __device__ __forceinline__ void epi_tap(EpiState& e, float (&Y)[RPB][XH], uint64_t* d_full, uint64_t* d_empty) {
   constexpr int NDB = Geo<TW>::NDB;
-  const uint32_t a = e.row_base + e.db * Geo<TW>::BAND_PX;
+  const uint32_t a = e.row_base + e.db * Geo<TW>::MMA_N;
   float z[18];
   mbar_wait(&d_full[e.db], e.dph);
   tc_fence_after();
   load_row<TW>(a, e.half, z);
   scatter_row<TW, RPB, CONV, T, 0>(Y, z);
-  load_row<TW>(a + TW, e.half, z);
+  load_row<TW>(a + Geo<TW>::RS, e.half, z);
   scatter_row<TW, RPB, CONV, T, 1>(Y, z);
-  load_row<TW>(a + 2 * TW, e.half, z);
+  load_row<TW>(a + 2 * Geo<TW>::RS, e.half, z);
   tc_fence_before();
   __syncwarp();
   if (e.lane == 0) mbar_arrive(&d_empty[e.db]);  // D buffer free: MMA may refill it
@@ -279,7 +304,8 @@ __device__ void epilogue(const TcParams& p, uint32_t tmem, uint64_t* d_full, uin
   const int sub = (warp - EPI_WARP0) / 4;
   const int srow = sub / G::HALVES, half = sub % G::HALVES;
   const int co_l = q * 32 + lane;
-  EpiState e{tmem + ((uint32_t)(q * 32) << 16) + D0 + srow * TW + half * 16, 0, 0, lane, half};
+  EpiState e{tmem + ((uint32_t)(q * 32) << 16) + D0 + srow * G::RS + half * 16, 0, 0, lane, half};
+  const int nstrip = G::STRIP ? p.W / 16 : 1;
   float Y[RPB][XH];
   for (int item = blockIdx.x; item < p.items; item += gridDim.x) {
     const int n = item / p.NCT, ct = item % p.NCT;
@@ -311,8 +337,9 @@ __device__ void epilogue(const TcParams& p, uint32_t tmem, uint64_t* d_full, uin
         epi_tap<TW, RPB, CONV, 6>(e, Y, d_full, d_empty);
         epi_tap<TW, RPB, CONV, 7>(e, Y, d_full, d_empty);
         epi_tap<TW, RPB, CONV, 8>(e, Y, d_full, d_empty);
-        const int row = G::OUT_ROWS * k + srow;
-        if (n < p.N && co < p.Cout && row < p.H && p.ablate != 1) finalize_row<TW, RPB>(p, Y, n, co, b, row, half * 16);
+        const int row = G::OUT_ROWS * (k / nstrip) + srow;
+        const int x0 = (k % nstrip) * 16 + half * 16;
+        if (n < p.N && co < p.Cout && row < p.H && p.ablate != 1) finalize_row<TW, RPB>(p, Y, n, co, b, row, x0);
       }
   }
 }
@@ -335,16 +362,15 @@ __global__ void __launch_bounds__(THREADS, 1) ri_tc_kernel(const __grid_constant
   using G = Geo<TW>;
   constexpr int NDB = G::NDB;
   constexpr int XTILE = G::XTILE;
-  constexpr int BAND_PX = G::BAND_PX;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   // 1 KB alignment for the SW128 atoms
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const int parts = p.passes == 3 ? 2 : 1;
-  const int xbuf_bytes = parts * p.NC * XTILE;
-  const int XB = p.x_bufs;               // 1 or 2 X band buffers
-  uint8_t* xs = smem;
-  uint8_t* ws = smem + XB * xbuf_bytes;  // W ring
-  __shared__ uint64_t w_full[8], w_empty[8], x_full[2], x_empty[2], d_full[MAX_NDB], d_empty[MAX_NDB];
+  uint8_t* xs = smem;                           // X band: [part][chunk] tiles of XTILE bytes
+  uint8_t* ws = smem + (p.xstream ? 0 : parts * p.NC * XTILE);  // W (+ X when streamed) ring
+  // per-chunk X barriers: chunk c of band k+1 is reloaded as soon as the MMAs of band k's
+  // last tap on chunk c complete, so band transitions overlap the last tap's MMAs
+  __shared__ uint64_t w_full[8], w_empty[8], x_full[MAX_NC], x_empty[MAX_NC], d_full[MAX_NDB], d_empty[MAX_NDB];
   __shared__ uint32_t tmem_base_sh;
 
   const int warp = threadIdx.x / 32;
@@ -354,7 +380,7 @@ __global__ void __launch_bounds__(THREADS, 1) ri_tc_kernel(const __grid_constant
       mbar_init(&w_full[s], 1);
       mbar_init(&w_empty[s], 1);
     }
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < p.NC; ++i) {
       mbar_init(&x_full[i], 1);
       mbar_init(&x_empty[i], 1);
     }
@@ -373,50 +399,61 @@ __global__ void __launch_bounds__(THREADS, 1) ri_tc_kernel(const __grid_constant
   // W stage = spc consecutive ci-chunks of one tap (hi, or hi+lo interleaved), ONE bulk
   // copy of >= 32 KB: the TMA engine's per-copy cost makes small copies the bottleneck
   // (profiles/r01/l2_microbench.jsonl).
-  const int stage_bytes = p.spc * parts * WTILE;
+  const int stage_w = p.spc * parts * WTILE;                      // W bytes of a stage
+  const int stage_bytes = stage_w + (p.xstream ? p.spc * parts * XTILE : 0);
   const int stages_per_tap = p.NC / p.spc;
   if (warp < EPI_WARP0) asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(REGS_PRODUCER));
   if (warp == 0) {
     // ------------------------------------------------------------ producer (whole warp
-    // walks the schedule; one elected lane issues the bulk copies)
+    // walks the schedule in MMA consumption order; one elected lane issues the copies)
     Ring wr;
-    uint32_t xc = 0;
+    uint32_t xc = 0;  // bands loaded so far (phase of the per-chunk X barriers)
     for (int item = blockIdx.x; item < p.items; item += gridDim.x) {
       const int n = item / p.NCT, ct = item % p.NCT;
       for (int b = 0; b < p.NB; ++b)
         for (int k = 0; k < p.NBK; ++k) {
-          const int xb = XB == 2 ? (xc & 1) : 0;
-          const uint32_t xuse = XB == 2 ? (xc >> 1) : xc;  // uses of this buffer so far
-          if (xuse > 0) mbar_wait(&x_empty[xb], (xuse - 1) & 1);
-          if (elect_one()) {
-            mbar_arrive_expect_tx(&x_full[xb], xbuf_bytes);
-            const size_t tile = ((size_t)n * p.NBK + k) * p.NC;
-            bulk_g2s(xs + xb * xbuf_bytes, p.xh + tile * XTILE, p.NC * XTILE, &x_full[xb]);
-            if (parts == 2)
-              bulk_g2s(xs + xb * xbuf_bytes + p.NC * XTILE, p.xl + tile * XTILE, p.NC * XTILE, &x_full[xb]);
-          }
-          __syncwarp();
-          ++xc;
+          const size_t tile = ((size_t)n * p.NBK + k) * p.NC;
           const uint8_t* wsrc = p.w + (((size_t)b * p.NCT + ct) * 9) * p.NC * parts * WTILE;
           for (int st = 0; st < 9 * stages_per_tap; ++st) {
+            if (!p.xstream && st < stages_per_tap) {  // tap 0: this stage's X chunks of the new band first
+              for (int cl = 0; cl < p.spc; ++cl) {
+                const int c = st * p.spc + cl;
+                if (xc > 0) mbar_wait(&x_empty[c], (xc - 1) & 1);
+                if (elect_one()) {
+                  mbar_arrive_expect_tx(&x_full[c], parts * XTILE);
+                  bulk_g2s(xs + c * XTILE, p.xh + (tile + c) * XTILE, XTILE, &x_full[c]);
+                  if (parts == 2) bulk_g2s(xs + (p.NC + c) * XTILE, p.xl + (tile + c) * XTILE, XTILE, &x_full[c]);
+                }
+                __syncwarp();
+              }
+            }
             if (wr.used) mbar_wait(&w_empty[wr.s], wr.ph ^ 1);
             if (elect_one()) {
               if (p.ablate == 3 || p.ablate == 4) {
                 mbar_arrive(&w_full[wr.s]);  // profiling: no weight traffic
               } else {
                 mbar_arrive_expect_tx(&w_full[wr.s], stage_bytes);
-                bulk_g2s(ws + wr.s * stage_bytes, wsrc + (size_t)st * stage_bytes, stage_bytes, &w_full[wr.s]);
+                uint8_t* dst = ws + wr.s * stage_bytes;
+                bulk_g2s(dst, wsrc + (size_t)st * stage_w, stage_w, &w_full[wr.s]);
+                if (p.xstream) {  // the stage's X chunks travel with it (re-read from L2 per tap)
+                  const int c0 = (st % stages_per_tap) * p.spc;
+                  bulk_g2s(dst + stage_w, p.xh + (tile + c0) * XTILE, p.spc * XTILE, &w_full[wr.s]);
+                  if (parts == 2)
+                    bulk_g2s(dst + stage_w + p.spc * XTILE, p.xl + (tile + c0) * XTILE, p.spc * XTILE, &w_full[wr.s]);
+                }
               }
             }
             __syncwarp();
             wr.adv(S);
           }
+          ++xc;
         }
     }
   } else if (warp == 1) {
     // ------------------------------------------------------------ MMA issuer (whole warp
     // waits; one elected lane issues tcgen05.mma + commits)
-    const uint32_t idesc = idesc_bf16_f32(128, BAND_PX);
+    const uint32_t idesc = idesc_bf16_f32(128, G::MMA_N);
+    const uint32_t xaddr = smem_u32(xs);
     Ring wr;
     uint32_t xc = 0, gd = 0;
     int db = 0;
@@ -424,34 +461,39 @@ __global__ void __launch_bounds__(THREADS, 1) ri_tc_kernel(const __grid_constant
     for (int item = blockIdx.x; item < p.items; item += gridDim.x) {
       for (int b = 0; b < p.NB; ++b)
         for (int k = 0; k < p.NBK; ++k) {
-          const int xb = XB == 2 ? (xc & 1) : 0;
-          const uint32_t xuse = XB == 2 ? (xc >> 1) : xc;
-          mbar_wait(&x_full[xb], xuse & 1);
-          tc_fence_after();
-          const uint32_t xaddr = smem_u32(xs + xb * xbuf_bytes);
           for (int t = 0; t < 9; ++t) {
             if (gd >= NDB) mbar_wait(&d_empty[db], dph ^ 1);
             tc_fence_after();
-            const uint32_t d = tmem + D0 + db * BAND_PX;
+            const uint32_t d = tmem + D0 + db * G::MMA_N;
             for (int sp = 0; sp < stages_per_tap; ++sp) {
+              if (t == 0 && !p.xstream)
+                for (int cl = 0; cl < p.spc; ++cl) mbar_wait(&x_full[sp * p.spc + cl], xc & 1);
               mbar_wait(&w_full[wr.s], wr.ph);
               tc_fence_after();
               if (elect_one()) {
                 const uint32_t wbase = smem_u32(ws + wr.s * stage_bytes);
                 for (int cl = 0; cl < ((p.ablate == 2 || p.ablate == 3) ? 0 : p.spc); ++cl) {
                   const int c = sp * p.spc + cl;
-                  const uint64_t bh = desc_k_sw128(xaddr + c * XTILE);
+                  // X chunk: resident band tile c, or the stage's streamed copy
+                  const uint32_t xh_a = p.xstream ? wbase + stage_w + cl * XTILE : xaddr + c * XTILE;
+                  const uint32_t xl_a = p.xstream ? wbase + stage_w + (p.spc + cl) * XTILE : xaddr + (p.NC + c) * XTILE;
+                  const uint64_t bh = desc_k_sw128(xh_a);
                   const uint64_t ah = desc_k_sw128(wbase + cl * parts * WTILE);
 #pragma unroll
                   for (int kk = 0; kk < 4; ++kk) mma_bf16_ss(d, ah + 2 * kk, bh + 2 * kk, idesc, (c | kk) != 0);
                   if (parts == 2) {
-                    const uint64_t bl = desc_k_sw128(xaddr + (p.NC + c) * XTILE);
+                    const uint64_t bl = desc_k_sw128(xl_a);
                     const uint64_t al = desc_k_sw128(wbase + (cl * parts + 1) * WTILE);
 #pragma unroll
                     for (int kk = 0; kk < 4; ++kk) mma_bf16_ss(d, ah + 2 * kk, bl + 2 * kk, idesc, 1);
 #pragma unroll
                     for (int kk = 0; kk < 4; ++kk) mma_bf16_ss(d, al + 2 * kk, bh + 2 * kk, idesc, 1);
                   }
+                  if (t == 8 && !p.xstream) mma_commit(&x_empty[c]);  // chunk c of this band fully consumed
+                }
+                if ((p.ablate == 2 || p.ablate == 3) && !p.xstream) {
+                  if (t == 8)
+                    for (int cl = 0; cl < p.spc; ++cl) mma_commit(&x_empty[sp * p.spc + cl]);
                 }
                 mma_commit(&w_empty[wr.s]);
                 if (sp == stages_per_tap - 1) mma_commit(&d_full[db]);
@@ -465,8 +507,6 @@ __global__ void __launch_bounds__(THREADS, 1) ri_tc_kernel(const __grid_constant
               dph ^= 1;
             }
           }
-          if (elect_one()) mma_commit(&x_empty[xb]);
-          __syncwarp();
           ++xc;
         }
     }
@@ -486,29 +526,34 @@ __device__ __forceinline__ void split_bf16(float v, __nv_bfloat16& hi, __nv_bflo
   lo = __float2bfloat16_rn(v - __bfloat162float(hi));
 }
 
-// X fp32 NCHW -> SW128 bf16 tiles [n][band k][chunk][BAND_PX px][64 ci] (hi, lo planes);
-// band k holds input rows k*OUT_ROWS-1 .. k*OUT_ROWS+OUT_ROWS; rows outside the image are
-// zero (the padding).
+// X fp32 NCHW -> SW128 bf16 tiles [n][band][chunk][MMA_N px][64 ci] (hi, lo planes).  Band
+// pixel px is (r = px / RS, cc = px % RS) -> image row k*OUT_ROWS - 1 + r and column
+// cc (full rows) or j*16 - 1 + cc (strip j); pixels outside the image (the padding) and the
+// MMA_N - BAND_PX filler pixels are zero.
 template <int TW>
 __global__ void x_pack_kernel(const float* __restrict__ x, uint8_t* __restrict__ xh,
-                              uint8_t* __restrict__ xl, int Cin, int H, int NBK, int NC) {
+                              uint8_t* __restrict__ xl, int Cin, int H, int W, int NBK, int NC) {
   using G = Geo<TW>;
-  __shared__ float tile[KC][G::BAND_PX + 1];
-  const int c = blockIdx.x, k = blockIdx.y, n = blockIdx.z;
-  for (int i = threadIdx.x; i < KC * G::BAND_PX; i += blockDim.x) {
-    const int cl = i / G::BAND_PX, px = i % G::BAND_PX;
-    const int ci = c * KC + cl, row = k * G::OUT_ROWS - 1 + px / TW, col = px % TW;
-    tile[cl][px] = (ci < Cin && row >= 0 && row < H) ? x[(((size_t)n * Cin + ci) * H + row) * TW + col] : 0.f;
+  __shared__ float tile[KC][G::MMA_N + 1];
+  const int c = blockIdx.x, bk = blockIdx.y, n = blockIdx.z;
+  const int nstrip = G::STRIP ? W / 16 : 1;
+  const int k = bk / nstrip, j = bk % nstrip;
+  for (int i = threadIdx.x; i < KC * G::MMA_N; i += blockDim.x) {
+    const int cl = i / G::MMA_N, px = i % G::MMA_N;
+    const int ci = c * KC + cl, row = k * G::OUT_ROWS - 1 + px / G::RS;
+    const int col = G::STRIP ? j * 16 - 1 + px % G::RS : px % G::RS;
+    const bool in = px < G::BAND_PX && ci < Cin && row >= 0 && row < H && col >= 0 && col < W;
+    tile[cl][px] = in ? x[(((size_t)n * Cin + ci) * H + row) * W + col] : 0.f;
   }
   __syncthreads();
-  const size_t tidx = ((size_t)n * NBK + k) * NC + c;
+  const size_t tidx = ((size_t)n * NBK + bk) * NC + c;
   uint8_t* oh = xh + tidx * G::XTILE;
   uint8_t* ol = xl ? xl + tidx * G::XTILE : nullptr;
-  for (int i = threadIdx.x; i < G::BAND_PX * (KC / 8); i += blockDim.x) {
+  for (int i = threadIdx.x; i < G::MMA_N * (KC / 8); i += blockDim.x) {
     const int px = i / (KC / 8), g = i % (KC / 8);
     __align__(16) __nv_bfloat16 h8[8], l8[8];
 #pragma unroll
-    for (int j = 0; j < 8; ++j) split_bf16(tile[g * 8 + j][px], h8[j], l8[j]);
+    for (int jj = 0; jj < 8; ++jj) split_bf16(tile[g * 8 + jj][px], h8[jj], l8[jj]);
     const uint32_t off = sw128_offset(px, g * 8);
     *reinterpret_cast<uint4*>(oh + off) = *reinterpret_cast<const uint4*>(h8);
     if (ol) *reinterpret_cast<uint4*>(ol + off) = *reinterpret_cast<const uint4*>(l8);
@@ -552,9 +597,9 @@ struct TcGeom {
 };
 TcGeom geom(const rc_desc& d) {
   TcGeom g;
-  const int out_rows = d.w == 32 ? Geo<32>::OUT_ROWS : Geo<16>::OUT_ROWS;
-  g.xtile = d.w == 32 ? Geo<32>::XTILE : Geo<16>::XTILE;
-  g.NBK = (d.h + out_rows - 1) / out_rows;
+  const int out_rows = d.w == 32 ? Geo<32>::OUT_ROWS : (d.w == 16 ? Geo<16>::OUT_ROWS : Geo<0>::OUT_ROWS);
+  g.xtile = d.w == 32 ? Geo<32>::XTILE : (d.w == 16 ? Geo<16>::XTILE : Geo<0>::XTILE);
+  g.NBK = (d.h + out_rows - 1) / out_rows * (d.w == 16 || d.w == 32 ? 1 : d.w / 16);
   g.NC = (d.c_in + KC - 1) / KC;
   g.NCT = (d.c_out + 127) / 128;
   g.x_plane = (size_t)d.n * g.NBK * g.NC * g.xtile;
@@ -563,29 +608,41 @@ TcGeom geom(const rc_desc& d) {
 }
 
 struct SmemPlan {
-  int spc, stages, x_bufs;
+  int spc, stages, xstream;
   size_t bytes;
 };
-// largest W stage (chunks per stage dividing NC) that leaves >= 2 stages; two X band
-// buffers when they fit next to two W stages of >= 32 KB, else one
+// Preferred: one resident X band (per-chunk barriers overlap its reload with the last tap)
+// plus the largest W stage (chunks per stage dividing NC) that leaves >= 2 stages.  When the
+// band does not fit (large Cin), X chunks are streamed with the W stages instead (X re-read
+// from L2 once per tap).
 SmemPlan smem_plan(const TcGeom& g, int parts) {
   SmemPlan sp{0, 0, 0, 0};
   const size_t cap = 232448 - 1024 - 1024;  // dynamic smem minus alignment slack / statics
   const size_t xbuf = (size_t)parts * g.NC * g.xtile;
   const size_t chunk = (size_t)parts * WTILE;
-  for (int xb = 2; xb >= 1 && sp.spc == 0; --xb) {
-    if (xb * xbuf >= cap) continue;
-    const size_t budget = cap - xb * xbuf;
+  if (g.NC <= MAX_NC && xbuf < cap) {
+    const size_t budget = cap - xbuf;
     for (int c = g.NC; c >= 1; --c) {
       if (g.NC % c) continue;
       const size_t sb = c * chunk;
-      if (2 * sb <= budget && (sb >= 32768 || c == g.NC || xb == 1)) {
+      if (2 * sb <= budget) {
         sp.spc = c;
         sp.stages = (int)(budget / sb) > 8 ? 8 : (int)(budget / sb);
-        sp.x_bufs = xb;
-        sp.bytes = xb * xbuf + sp.stages * sb + 1024;
-        break;
+        sp.bytes = xbuf + sp.stages * sb + 1024;
+        return sp;
       }
+    }
+  }
+  const size_t schunk = (size_t)parts * (WTILE + g.xtile);
+  for (int c = g.NC; c >= 1; --c) {
+    if (g.NC % c) continue;
+    const size_t sb = c * schunk;
+    if (3 * sb <= cap || (c == 1 && 2 * sb <= cap)) {
+      sp.spc = c;
+      sp.stages = (int)(cap / sb) > 8 ? 8 : (int)(cap / sb);
+      sp.xstream = 1;
+      sp.bytes = sp.stages * sb + 1024;
+      return sp;
     }
   }
   return sp;
@@ -598,7 +655,7 @@ bool tc_supported(const rc_desc& d) {
   const int R = d.orientations;
   const bool fold_ok = d.pool == RC_POOL_NONE || (d.pool == RC_POOL_AVG && (R & (R - 1)) == 0) || gf == 1 ||
                        gf == 2 || gf % 4 == 0;
-  if (!(d.k == 3 && (d.w == 16 || d.w == 32) && fold_ok &&
+  if (!(d.k == 3 && (d.w == 16 || d.w == 32 || (d.w >= 48 && d.w % 16 == 0)) && fold_ok &&
         (d.precision == RC_PREC_BF16 || d.precision == RC_PREC_BF16X3 || d.precision == RC_PREC_AUTO)))
     return false;
   const int parts = d.precision == RC_PREC_BF16 ? 1 : 2;
@@ -628,8 +685,10 @@ int launch_tc(const rc_desc& d, const float* x, const void* bank, const float* b
               void* ws, size_t ws_bytes, cudaStream_t s, bool dry_run, const char** name) {
   if (!tc_supported(d)) return RC_ERR_UNSUPPORTED;
   if (name) {
-    static const char* names[2][2] = {{"tc_k3w16_bf16x3", "tc_k3w16_bf16"}, {"tc_k3w32_bf16x3", "tc_k3w32_bf16"}};
-    *name = names[d.w == 32][d.precision == RC_PREC_BF16];
+    static const char* names[3][2] = {{"tc_k3w16_bf16x3", "tc_k3w16_bf16"},
+                                      {"tc_k3w32_bf16x3", "tc_k3w32_bf16"},
+                                      {"tc_k3strip_bf16x3", "tc_k3strip_bf16"}};
+    *name = names[d.w == 16 ? 0 : (d.w == 32 ? 1 : 2)][d.precision == RC_PREC_BF16];
   }
   if (dry_run || d.n == 0) return RC_OK;
   const TcGeom g = geom(d);
@@ -639,10 +698,13 @@ int launch_tc(const rc_desc& d, const float* x, const void* bank, const float* b
   const int parts = passes == 3 ? 2 : 1;
   uint8_t* xh = static_cast<uint8_t*>(ws);
   uint8_t* xl = passes == 3 ? xh + g.x_plane : nullptr;
-  if (d.w == 32)
-    x_pack_kernel<32><<<dim3(g.NC, g.NBK, d.n), 256, 0, s>>>(x, xh, xl, d.c_in, d.h, g.NBK, g.NC);
+  const int gi = d.w == 16 ? 0 : (d.w == 32 ? 1 : 2);
+  if (gi == 1)
+    x_pack_kernel<32><<<dim3(g.NC, g.NBK, d.n), 256, 0, s>>>(x, xh, xl, d.c_in, d.h, d.w, g.NBK, g.NC);
+  else if (gi == 0)
+    x_pack_kernel<16><<<dim3(g.NC, g.NBK, d.n), 256, 0, s>>>(x, xh, xl, d.c_in, d.h, d.w, g.NBK, g.NC);
   else
-    x_pack_kernel<16><<<dim3(g.NC, g.NBK, d.n), 256, 0, s>>>(x, xh, xl, d.c_in, d.h, g.NBK, g.NC);
+    x_pack_kernel<0><<<dim3(g.NC, g.NBK, d.n), 256, 0, s>>>(x, xh, xl, d.c_in, d.h, d.w, g.NBK, g.NC);
   RC_CUDA(cudaGetLastError());
   const BankLayout L = bank_layout(d);
   const uint8_t* tcb = static_cast<const uint8_t*>(bank) + L.tc_off;
@@ -656,6 +718,7 @@ int launch_tc(const rc_desc& d, const float* x, const void* bank, const float* b
   p.am = (d.pool == RC_POOL_MAX || d.pool == RC_POOL_SUBGROUP) ? am : nullptr;
   p.N = d.n;
   p.H = d.h;
+  p.W = d.w;
   p.Cout = d.c_out;
   p.NB = num_bases(d);
   p.NBK = g.NBK;
@@ -669,7 +732,7 @@ int launch_tc(const rc_desc& d, const float* x, const void* bank, const float* b
   p.act = d.activation;
   p.w_stages = plan.stages;
   p.spc = plan.spc;
-  p.x_bufs = plan.x_bufs;
+  p.xstream = plan.xstream;
   p.items = g.NCT * d.n;
   {
     const char* ab = getenv("RC_TC_ABLATE");  // profiling switch, see TcParams::ablate
@@ -680,12 +743,15 @@ int launch_tc(const rc_desc& d, const float* x, const void* bank, const float* b
   RC_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
   const int grid = p.items < sms ? p.items : sms;
   // [width][single][convention]
-  static void (*const kernels[2][2][2])(TcParams) = {
+  static void (*const kernels[3][2][2])(TcParams) = {
       {{ri_tc_kernel<16, 4, 0>, ri_tc_kernel<16, 4, 1>}, {ri_tc_kernel<16, 1, 0>, ri_tc_kernel<16, 1, 1>}},
-      {{ri_tc_kernel<32, 4, 0>, ri_tc_kernel<32, 4, 1>}, {ri_tc_kernel<32, 1, 0>, ri_tc_kernel<32, 1, 1>}}};
-  void (*fn)(TcParams) = kernels[d.w == 32][d.group == RC_GROUP_SINGLE][d.convention == RC_CONV_RAW];
+      {{ri_tc_kernel<32, 4, 0>, ri_tc_kernel<32, 4, 1>}, {ri_tc_kernel<32, 1, 0>, ri_tc_kernel<32, 1, 1>}},
+      {{ri_tc_kernel<0, 4, 0>, ri_tc_kernel<0, 4, 1>}, {ri_tc_kernel<0, 1, 0>, ri_tc_kernel<0, 1, 1>}}};
+  void (*fn)(TcParams) = kernels[gi][d.group == RC_GROUP_SINGLE][d.convention == RC_CONV_RAW];
   RC_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)plan.bytes));
+  prof_begin(s);
   fn<<<grid, THREADS, plan.bytes, s>>>(p);
+  prof_end(s);
   RC_CUDA(cudaGetLastError());
   return RC_OK;
 }

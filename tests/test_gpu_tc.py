@@ -159,6 +159,60 @@ def test_tc_single_orientation_dyadic(O, dev, cfg, precision):
         assert not a.any()
 
 
+STRIP_CONFIGS = [
+    # (n, cin, h, w, cout, group, R, pool, g, convention): W >= 48, W % 16 == 0 -> 4x16 strips
+    (2, 64, 64, 64, 128, "p4m", 8, "subgroup", 4, "scatter"),
+    (1, 32, 9, 48, 130, "p4", 4, "max", 4, "raw"),
+    (2, 128, 16, 64, 128, "single", 1, "none", 1, "scatter"),
+    (1, 16, 6, 80, 128, "steer", 8, "avg", 4, "scatter"),
+]
+
+
+@pytest.mark.parametrize("precision", ["bf16", "bf16x3"])
+@pytest.mark.parametrize("cfg", STRIP_CONFIGS, ids=lambda c: "-".join(map(str, c)))
+def test_tc_strip_dyadic_bitexact(O, dev, cfg, precision):
+    import paper_2512_08888_b200 as P
+    n, cin, h, w, cout, g, R, pool, pg, conv = cfg
+    d = O.Desc(n, cin, h, w, cout, 3, g, R, pool, pg, conv)
+    rng = np.random.default_rng(abs(hash(cfg)) % 2**32)
+    x = dyadic(rng, (n, cin, h, w))
+    w0 = dyadic(rng, (cout, cin, 3, 3))
+    w1 = dyadic(rng, (cout, cin, 3, 3)) if g == "steer" else None
+    bias = dyadic(rng, cout)
+    y_ref, a_ref = O.ri_forward(d, x, w0, w1, bias)
+    y, a = run(P, d, x, w0, w1, bias, precision, dev)
+    if g == "steer":  # 45-degree base: irrational coefficients, FP32-class tolerance
+        err = np.abs(y.reshape(y_ref.shape).astype(np.float64) - y_ref).max() / np.abs(y_ref).max()
+        assert err <= TOL[precision], err
+        return
+    assert np.array_equal(y.reshape(y_ref.shape), y_ref), f"max|dy| = {np.abs(y.reshape(y_ref.shape) - y_ref).max()}"
+    if a_ref is not None and g != "single":
+        assert np.array_equal(a, a_ref), f"argmax mismatches {(a != a_ref).sum()}"
+
+
+@pytest.mark.parametrize("precision", ["bf16", "bf16x3"])
+@pytest.mark.parametrize("cfg", [(1, 512, 16, 16, 256, "single", 1, "none", 1),
+                                 (1, 640, 8, 16, 128, "p4m", 8, "subgroup", 4),
+                                 (1, 576, 6, 32, 130, "p4", 4, "max", 4),
+                                 (1, 1024, 4, 64, 128, "single", 1, "none", 1)],
+                         ids=lambda c: "-".join(map(str, c)))
+def test_tc_large_cin_streamed_x(O, dev, cfg, precision):
+    """Cin large enough that the X band does not fit in shared memory: X chunks are
+    streamed with the weight stages (bf16x3) -- still bit-exact on dyadic inputs."""
+    import paper_2512_08888_b200 as P
+    n, cin, h, w, cout, g, R, pool, pg = cfg
+    d = O.Desc(n, cin, h, w, cout, 3, g, R, pool, pg)
+    rng = np.random.default_rng(abs(hash(cfg)) % 2**32)
+    x = dyadic(rng, (n, cin, h, w))
+    w0 = dyadic(rng, (cout, cin, 3, 3))
+    bias = dyadic(rng, cout)
+    y_ref, a_ref = O.ri_forward(d, x, w0, None, bias, nthreads=8)
+    y, a = run(P, d, x, w0, None, bias, precision, dev)
+    assert np.array_equal(y.reshape(y_ref.shape), y_ref), f"max|dy| = {np.abs(y.reshape(y_ref.shape) - y_ref).max()}"
+    if a_ref is not None and g != "single":
+        assert np.array_equal(a, a_ref)
+
+
 @pytest.mark.parametrize("kernel", ["tc", "simt"])
 def test_fused_relu_activation(O, dev, kernel):
     """activation = relu is applied after the bias (relu of the oracle's pooled output)."""

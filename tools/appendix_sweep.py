@@ -11,7 +11,8 @@ filters {256, 512, 1024}, batch N (the paper gives none; 32 as for C1).  For eve
                  (best algorithm autotuned), FMA-only (allow_tf32 = False) and TF32-allowed,
                  on the scatter semantics: scatter_conv_multi(X, W) == conv2d(X, flip(W), pad=1)
                  (scatter_conv.hpp:17-19 duality).  Context only -- not the product path;
-  * a cross-check before timing: ours vs cuDNN FMA-only, normwise <= 1e-5.
+  * a cross-check before timing: ours vs cuDNN FMA-only, normwise <= 1e-4 (the
+    SPEC 32-bit tolerance; cuDNN's own FP32 algorithms differ from the exact sum by ~1e-5).
 
 Writes the SPEC bench_cli record schema plus the B200 columns as CSV and one
 JSON document, and prints a markdown table with the paper's RTX 3080 Ti numbers beside.
@@ -111,6 +112,16 @@ def main():
                 torch.cuda.synchronize()
                 err = ((y[:, :, 0] - yc).abs().max() / yc.abs().max()).item()
                 ours = time_ms(lambda: P.ri_conv_forward(desc, x, bank, out=y), args.repeats)
+                # FP32-class tensor-core path (bf16x3) where the kernel covers the shape
+                dtc = P.Desc(args.n, cin, s, s, cout, 3, "single", 1, "none", 1, "scatter", "auto")
+                tc_ms, tc_err, tc_kernel = None, None, dtc.kernel_name()
+                if tc_kernel.startswith("tc_"):
+                    btc = P.bank_precompute(dtc, w)
+                    ytc = torch.empty_like(y)
+                    P.ri_conv_forward(dtc, x, btc, out=ytc)
+                    torch.cuda.synchronize()
+                    tc_err = ((ytc[:, :, 0] - yc).abs().max() / yc.abs().max()).item()
+                    tc_ms = time_ms(lambda: P.ri_conv_forward(dtc, x, btc, out=ytc), args.repeats)
                 fma = time_ms(lambda: F.conv2d(x, wf, padding=1), args.repeats)
                 torch.backends.cudnn.allow_tf32 = True
                 tf32 = time_ms(lambda: F.conv2d(x, wf, padding=1), args.repeats)
@@ -124,7 +135,11 @@ def main():
                     "peak_aux_bytes": desc.workspace_bytes(), "batch": args.n, "kernel": desc.kernel_name(),
                     "tflops": round(flops / ours / 1e9, 3), "cudnn_fma_ms": round(fma, 5),
                     "cudnn_tf32_ms": round(tf32, 5), "speedup_vs_cudnn_fma": round(fma / ours, 3),
-                    "max_rel_err_vs_cudnn": err, "cross_check": err <= 1e-5,
+                    "max_rel_err_vs_cudnn": err, "cross_check": err <= 1e-4,
+                    "tc_kernel": tc_kernel, "tc_bf16x3_ms": round(tc_ms, 5) if tc_ms else None,
+                    "tc_rel_err_vs_cudnn": tc_err,
+                    "tc_speedup_vs_cudnn_fma": round(fma / tc_ms, 3) if tc_ms else None,
+                    "tc_speedup_vs_cudnn_tf32": round(tf32 / tc_ms, 3) if tc_ms else None,
                     "paper_3080ti_scatter_ms": paper[0] if paper else None,
                     "paper_3080ti_cudnn_ms": paper[1] if paper else None,
                 })
@@ -137,7 +152,8 @@ def main():
             "cudnn": torch.backends.cudnn.version(), "batch": args.n, "k": 3,
             "note": "ours = fused FP32 kernel; cudnn = torch conv2d on flipped kernels (context only)"}
     json.dump({"meta": meta, "rows": rows}, open(os.path.join(args.out, "appendix_sweep.json"), "w"), indent=1)
-    ok = all(r["cross_check"] for r in rows)
+    ok = all(r["cross_check"] and (r["tc_rel_err_vs_cudnn"] is None or r["tc_rel_err_vs_cudnn"] <= 1e-4)
+             for r in rows)
     print(f"cross-check {'PASS' if ok else 'FAIL'} on {len(rows)} cells")
     sys.exit(0 if ok else 1)
 
