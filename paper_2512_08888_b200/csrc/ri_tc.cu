@@ -269,15 +269,19 @@ struct EpiState {
   int db;
   uint32_t dph;
   int lane, half;
+  uint32_t dempty_cl;  // CTA pairs: shared::cluster address of the leader's d_empty[0]
 };
 
 // one tap (compile-time T): three single-row TMEM round trips, D released after the last
-template <int TW, int RPB, int CONV, int T>
+template <int TW, int RPB, int CONV, int T, bool PAIR>
 __device__ __forceinline__ void epi_tap(EpiState& e, float (&Y)[RPB][XH], uint64_t* d_full, uint64_t* d_empty) {
   constexpr int NDB = Geo<TW>::NDB;
   const uint32_t a = e.row_base + e.db * Geo<TW>::MMA_N;
   float z[18];
-  mbar_wait(&d_full[e.db], e.dph);
+  if constexpr (PAIR)
+    mbar_wait_spin(&d_full[e.db], e.dph);  // pairs: arrived by the leader's multicast commit
+  else
+    mbar_wait(&d_full[e.db], e.dph);
   tc_fence_after();
   load_row<TW>(a, e.half, z);
   scatter_row<TW, RPB, CONV, T, 0>(Y, z);
@@ -286,7 +290,12 @@ __device__ __forceinline__ void epi_tap(EpiState& e, float (&Y)[RPB][XH], uint64
   load_row<TW>(a + 2 * Geo<TW>::RS, e.half, z);
   tc_fence_before();
   __syncwarp();
-  if (e.lane == 0) mbar_arrive(&d_empty[e.db]);  // D buffer free: MMA may refill it
+  if (e.lane == 0) {  // D buffer free: the MMA may refill it (pairs: the leader's barrier)
+    if constexpr (PAIR)
+      mbar_arrive_cluster(e.dempty_cl + e.db * 8);
+    else
+      mbar_arrive(&d_empty[e.db]);
+  }
   if (++e.db == NDB) {
     e.db = 0;
     e.dph ^= 1;
@@ -296,7 +305,22 @@ __device__ __forceinline__ void epi_tap(EpiState& e, float (&Y)[RPB][XH], uint64
 
 // Epilogue warp: lane quadrant q (co = q*32 + lane); sub-tile sub = (output row of the
 // band, column half): TW = 16 -> 4 rows x 1 half, TW = 32 -> 2 rows x 2 halves.
-template <int TW, int RPB, int CONV>
+// Work schedule: item -> (image n, co tile ct).  Single CTAs walk items n*NCT + ct; CTA
+// pairs walk pair items n*(NCT/2) + ctp and CTA rank r of the pair takes ct = 2*ctp + r.
+struct Work {
+  int first, stride, count, per_n, rank;
+  __device__ __forceinline__ int n(int item) const { return item / per_n; }
+  __device__ __forceinline__ int ct(int item) const { return rank < 0 ? item % per_n : 2 * (item % per_n) + rank; }
+};
+template <bool PAIR>
+__device__ __forceinline__ Work make_work(const TcParams& p) {
+  if constexpr (PAIR)
+    return Work{(int)cluster_id_x(), (int)ncluster_x(), p.N * (p.NCT / 2), p.NCT / 2, (int)cluster_ctarank()};
+  else
+    return Work{(int)blockIdx.x, (int)gridDim.x, p.items, p.NCT, -1};
+}
+
+template <int TW, int RPB, int CONV, bool PAIR>
 __device__ void epilogue(const TcParams& p, uint32_t tmem, uint64_t* d_full, uint64_t* d_empty) {
   using G = Geo<TW>;
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
@@ -304,17 +328,24 @@ __device__ void epilogue(const TcParams& p, uint32_t tmem, uint64_t* d_full, uin
   const int sub = (warp - EPI_WARP0) / 4;
   const int srow = sub / G::HALVES, half = sub % G::HALVES;
   const int co_l = q * 32 + lane;
-  EpiState e{tmem + ((uint32_t)(q * 32) << 16) + D0 + srow * G::RS + half * 16, 0, 0, lane, half};
+  EpiState e{tmem + ((uint32_t)(q * 32) << 16) + D0 + srow * G::RS + half * 16, 0, 0, lane, half,
+             PAIR ? mapa_shared(d_empty, 0) : 0u};
   const int nstrip = G::STRIP ? p.W / 16 : 1;
   float Y[RPB][XH];
-  for (int item = blockIdx.x; item < p.items; item += gridDim.x) {
-    const int n = item / p.NCT, ct = item % p.NCT;
+  const Work wk = make_work<PAIR>(p);
+  for (int item = wk.first; item < wk.count; item += wk.stride) {
+    const int n = wk.n(item), ct = wk.ct(item);
     const int co = ct * 128 + co_l;
     if (p.ablate == 5) {  // profiling: consume D buffers without reading them
       for (int i = 0; i < p.NB * p.NBK * 9; ++i) {
         mbar_wait(&d_full[e.db], e.dph);
         __syncwarp();
-        if (lane == 0) mbar_arrive(&d_empty[e.db]);
+        if (lane == 0) {
+          if constexpr (PAIR)
+            mbar_arrive_cluster(e.dempty_cl + e.db * 8);
+          else
+            mbar_arrive(&d_empty[e.db]);
+        }
         if (++e.db == G::NDB) {
           e.db = 0;
           e.dph ^= 1;
@@ -328,15 +359,15 @@ __device__ void epilogue(const TcParams& p, uint32_t tmem, uint64_t* d_full, uin
         for (int r = 0; r < RPB; ++r)
 #pragma unroll
           for (int x = 0; x < XH; ++x) Y[r][x] = 0.f;
-        epi_tap<TW, RPB, CONV, 0>(e, Y, d_full, d_empty);
-        epi_tap<TW, RPB, CONV, 1>(e, Y, d_full, d_empty);
-        epi_tap<TW, RPB, CONV, 2>(e, Y, d_full, d_empty);
-        epi_tap<TW, RPB, CONV, 3>(e, Y, d_full, d_empty);
-        epi_tap<TW, RPB, CONV, 4>(e, Y, d_full, d_empty);
-        epi_tap<TW, RPB, CONV, 5>(e, Y, d_full, d_empty);
-        epi_tap<TW, RPB, CONV, 6>(e, Y, d_full, d_empty);
-        epi_tap<TW, RPB, CONV, 7>(e, Y, d_full, d_empty);
-        epi_tap<TW, RPB, CONV, 8>(e, Y, d_full, d_empty);
+        epi_tap<TW, RPB, CONV, 0, PAIR>(e, Y, d_full, d_empty);
+        epi_tap<TW, RPB, CONV, 1, PAIR>(e, Y, d_full, d_empty);
+        epi_tap<TW, RPB, CONV, 2, PAIR>(e, Y, d_full, d_empty);
+        epi_tap<TW, RPB, CONV, 3, PAIR>(e, Y, d_full, d_empty);
+        epi_tap<TW, RPB, CONV, 4, PAIR>(e, Y, d_full, d_empty);
+        epi_tap<TW, RPB, CONV, 5, PAIR>(e, Y, d_full, d_empty);
+        epi_tap<TW, RPB, CONV, 6, PAIR>(e, Y, d_full, d_empty);
+        epi_tap<TW, RPB, CONV, 7, PAIR>(e, Y, d_full, d_empty);
+        epi_tap<TW, RPB, CONV, 8, PAIR>(e, Y, d_full, d_empty);
         const int row = G::OUT_ROWS * (k / nstrip) + srow;
         const int x0 = (k % nstrip) * 16 + half * 16;
         if (n < p.N && co < p.Cout && row < p.H && p.ablate != 1) finalize_row<TW, RPB>(p, Y, n, co, b, row, x0);
@@ -357,42 +388,59 @@ struct Ring {
   }
 };
 
-template <int TW, int RPB, int CONV>
+// PAIR: a cluster of 2 CTAs issues M = 256 MMAs (tcgen05 cta_group::2) -- each CTA
+// supplies the weights of its own 128 output channels and HALF of the X band, so the
+// shared-memory operand traffic per MMA drops from 4 KB + N*32 B to 4 KB + N*16 B and the
+// N = 96 band MMA becomes math-bound.  The leader (rank 0) issues the MMAs; the peer's MMA
+// warp forwards "stage loaded" events to the leader; commits multicast to both CTAs; both
+// epilogues release D buffers on the leader's barrier.
+template <int TW, int RPB, int CONV, bool PAIR>
 __global__ void __launch_bounds__(THREADS, 1) ri_tc_kernel(const __grid_constant__ TcParams p) {
   using G = Geo<TW>;
   constexpr int NDB = G::NDB;
-  constexpr int XTILE = G::XTILE;
+  constexpr int XTILE = G::XTILE;                     // bytes of a full band tile (global layout)
+  constexpr int XS = PAIR ? XTILE / 2 : XTILE;        // bytes of this CTA's part of it in smem
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   // 1 KB alignment for the SW128 atoms
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const int parts = p.passes == 3 ? 2 : 1;
-  uint8_t* xs = smem;                           // X band: [part][chunk] tiles of XTILE bytes
-  uint8_t* ws = smem + (p.xstream ? 0 : parts * p.NC * XTILE);  // W (+ X when streamed) ring
+  uint8_t* xs = smem;                           // X band: [part][chunk] tiles of XS bytes
+  uint8_t* ws = smem + (p.xstream ? 0 : parts * p.NC * XS);  // W (+ X when streamed) ring
   // per-chunk X barriers: chunk c of band k+1 is reloaded as soon as the MMAs of band k's
   // last tap on chunk c complete, so band transitions overlap the last tap's MMAs
   __shared__ uint64_t w_full[8], w_empty[8], x_full[MAX_NC], x_empty[MAX_NC], d_full[MAX_NDB], d_empty[MAX_NDB];
+  __shared__ uint64_t pw_full[8], px_full[MAX_NC];  // pairs: the peer's loads, forwarded to the leader
   __shared__ uint32_t tmem_base_sh;
 
   const int warp = threadIdx.x / 32;
   const int S = p.w_stages;
+  const uint32_t rank = PAIR ? cluster_ctarank() : 0;
   if (threadIdx.x == 0) {
     for (int s = 0; s < S; ++s) {
       mbar_init(&w_full[s], 1);
       mbar_init(&w_empty[s], 1);
+      mbar_init(&pw_full[s], 1);
     }
     for (int i = 0; i < p.NC; ++i) {
       mbar_init(&x_full[i], 1);
       mbar_init(&x_empty[i], 1);
+      mbar_init(&px_full[i], 1);
     }
     for (int i = 0; i < NDB; ++i) {
       mbar_init(&d_full[i], 1);
-      mbar_init(&d_empty[i], NUM_EPI);
+      mbar_init(&d_empty[i], PAIR ? 2 * NUM_EPI : NUM_EPI);
     }
     fence_barrier_init();
   }
-  if (warp == 1) tmem_alloc<512>(&tmem_base_sh);
+  if (warp == 1) {
+    if constexpr (PAIR)
+      tmem_alloc2<512>(&tmem_base_sh);
+    else
+      tmem_alloc<512>(&tmem_base_sh);
+  }
   tc_fence_before();
   __syncthreads();
+  if constexpr (PAIR) cluster_sync_all();  // peer barriers initialised before any remote arrive
   tc_fence_after();
   const uint32_t tmem = tmem_base_sh;
 
@@ -400,16 +448,18 @@ __global__ void __launch_bounds__(THREADS, 1) ri_tc_kernel(const __grid_constant
   // copy of >= 32 KB: the TMA engine's per-copy cost makes small copies the bottleneck
   // (profiles/r01/l2_microbench.jsonl).
   const int stage_w = p.spc * parts * WTILE;                      // W bytes of a stage
-  const int stage_bytes = stage_w + (p.xstream ? p.spc * parts * XTILE : 0);
+  const int stage_bytes = stage_w + (p.xstream ? p.spc * parts * XS : 0);
   const int stages_per_tap = p.NC / p.spc;
+  const Work wk = make_work<PAIR>(p);
+  const size_t xoff = PAIR ? rank * XS : 0;  // this CTA's half of every band tile
   if (warp < EPI_WARP0) asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(REGS_PRODUCER));
   if (warp == 0) {
     // ------------------------------------------------------------ producer (whole warp
     // walks the schedule in MMA consumption order; one elected lane issues the copies)
     Ring wr;
     uint32_t xc = 0;  // bands loaded so far (phase of the per-chunk X barriers)
-    for (int item = blockIdx.x; item < p.items; item += gridDim.x) {
-      const int n = item / p.NCT, ct = item % p.NCT;
+    for (int item = wk.first; item < wk.count; item += wk.stride) {
+      const int n = wk.n(item), ct = wk.ct(item);
       for (int b = 0; b < p.NB; ++b)
         for (int k = 0; k < p.NBK; ++k) {
           const size_t tile = ((size_t)n * p.NBK + k) * p.NC;
@@ -418,16 +468,26 @@ __global__ void __launch_bounds__(THREADS, 1) ri_tc_kernel(const __grid_constant
             if (!p.xstream && st < stages_per_tap) {  // tap 0: this stage's X chunks of the new band first
               for (int cl = 0; cl < p.spc; ++cl) {
                 const int c = st * p.spc + cl;
-                if (xc > 0) mbar_wait(&x_empty[c], (xc - 1) & 1);
+                if (xc > 0) {
+                  if constexpr (PAIR)
+                    mbar_wait_spin(&x_empty[c], (xc - 1) & 1);
+                  else
+                    mbar_wait(&x_empty[c], (xc - 1) & 1);
+                }
                 if (elect_one()) {
-                  mbar_arrive_expect_tx(&x_full[c], parts * XTILE);
-                  bulk_g2s(xs + c * XTILE, p.xh + (tile + c) * XTILE, XTILE, &x_full[c]);
-                  if (parts == 2) bulk_g2s(xs + (p.NC + c) * XTILE, p.xl + (tile + c) * XTILE, XTILE, &x_full[c]);
+                  mbar_arrive_expect_tx(&x_full[c], parts * XS);
+                  bulk_g2s(xs + c * XS, p.xh + (tile + c) * XTILE + xoff, XS, &x_full[c]);
+                  if (parts == 2) bulk_g2s(xs + (p.NC + c) * XS, p.xl + (tile + c) * XTILE + xoff, XS, &x_full[c]);
                 }
                 __syncwarp();
               }
             }
-            if (wr.used) mbar_wait(&w_empty[wr.s], wr.ph ^ 1);
+            if (wr.used) {
+              if constexpr (PAIR)
+                mbar_wait_spin(&w_empty[wr.s], wr.ph ^ 1);
+              else
+                mbar_wait(&w_empty[wr.s], wr.ph ^ 1);
+            }
             if (elect_one()) {
               if (p.ablate == 3 || p.ablate == 4) {
                 mbar_arrive(&w_full[wr.s]);  // profiling: no weight traffic
@@ -437,9 +497,12 @@ __global__ void __launch_bounds__(THREADS, 1) ri_tc_kernel(const __grid_constant
                 bulk_g2s(dst, wsrc + (size_t)st * stage_w, stage_w, &w_full[wr.s]);
                 if (p.xstream) {  // the stage's X chunks travel with it (re-read from L2 per tap)
                   const int c0 = (st % stages_per_tap) * p.spc;
-                  bulk_g2s(dst + stage_w, p.xh + (tile + c0) * XTILE, p.spc * XTILE, &w_full[wr.s]);
-                  if (parts == 2)
-                    bulk_g2s(dst + stage_w + p.spc * XTILE, p.xl + (tile + c0) * XTILE, p.spc * XTILE, &w_full[wr.s]);
+                  for (int cl = 0; cl < p.spc; ++cl) {
+                    bulk_g2s(dst + stage_w + cl * XS, p.xh + (tile + c0 + cl) * XTILE + xoff, XS, &w_full[wr.s]);
+                    if (parts == 2)
+                      bulk_g2s(dst + stage_w + (p.spc + cl) * XS, p.xl + (tile + c0 + cl) * XTILE + xoff, XS,
+                               &w_full[wr.s]);
+                  }
                 }
               }
             }
@@ -449,54 +512,118 @@ __global__ void __launch_bounds__(THREADS, 1) ri_tc_kernel(const __grid_constant
           ++xc;
         }
     }
+  } else if (warp == 1 && PAIR && rank != 0) {
+    // ------------------------------------------------------------ pair peer: forward
+    // "this CTA's stage / X chunk landed" to the leader, in the leader's consumption order
+    const uint32_t pw_cl = mapa_shared(pw_full, 0), px_cl = mapa_shared(px_full, 0);
+    Ring wr;
+    uint32_t xc = 0;
+    for (int item = wk.first; item < wk.count; item += wk.stride)
+      for (int b = 0; b < p.NB; ++b)
+        for (int k = 0; k < p.NBK; ++k) {
+          for (int t = 0; t < 9; ++t)
+            for (int sp = 0; sp < stages_per_tap; ++sp) {
+              if (t == 0 && !p.xstream)
+                for (int cl = 0; cl < p.spc; ++cl) {
+                  const int c = sp * p.spc + cl;
+                  mbar_wait(&x_full[c], xc & 1);
+                  if (elect_one()) mbar_arrive_cluster(px_cl + c * 8);
+                  __syncwarp();
+                }
+              mbar_wait(&w_full[wr.s], wr.ph);
+              if (elect_one()) mbar_arrive_cluster(pw_cl + wr.s * 8);
+              __syncwarp();
+              wr.adv(S);
+            }
+          ++xc;
+        }
   } else if (warp == 1) {
     // ------------------------------------------------------------ MMA issuer (whole warp
     // waits; one elected lane issues tcgen05.mma + commits)
-    const uint32_t idesc = idesc_bf16_f32(128, G::MMA_N);
+    const uint32_t idesc = idesc_bf16_f32(PAIR ? 256 : 128, G::MMA_N);
     const uint32_t xaddr = smem_u32(xs);
     Ring wr;
     uint32_t xc = 0, gd = 0;
     int db = 0;
     uint32_t dph = 0;
-    for (int item = blockIdx.x; item < p.items; item += gridDim.x) {
+    for (int item = wk.first; item < wk.count; item += wk.stride) {
       for (int b = 0; b < p.NB; ++b)
         for (int k = 0; k < p.NBK; ++k) {
           for (int t = 0; t < 9; ++t) {
-            if (gd >= NDB) mbar_wait(&d_empty[db], dph ^ 1);
+            if (gd >= NDB) {
+              if constexpr (PAIR)
+                mbar_wait_spin(&d_empty[db], dph ^ 1);  // completed by the peer's epilogue too
+              else
+                mbar_wait(&d_empty[db], dph ^ 1);
+            }
             tc_fence_after();
             const uint32_t d = tmem + D0 + db * G::MMA_N;
             for (int sp = 0; sp < stages_per_tap; ++sp) {
               if (t == 0 && !p.xstream)
-                for (int cl = 0; cl < p.spc; ++cl) mbar_wait(&x_full[sp * p.spc + cl], xc & 1);
+                for (int cl = 0; cl < p.spc; ++cl) {
+                  mbar_wait(&x_full[sp * p.spc + cl], xc & 1);
+                  if constexpr (PAIR) mbar_wait_spin(&px_full[sp * p.spc + cl], xc & 1);
+                }
               mbar_wait(&w_full[wr.s], wr.ph);
+              if constexpr (PAIR) mbar_wait_spin(&pw_full[wr.s], wr.ph);
               tc_fence_after();
               if (elect_one()) {
                 const uint32_t wbase = smem_u32(ws + wr.s * stage_bytes);
                 for (int cl = 0; cl < ((p.ablate == 2 || p.ablate == 3) ? 0 : p.spc); ++cl) {
                   const int c = sp * p.spc + cl;
                   // X chunk: resident band tile c, or the stage's streamed copy
-                  const uint32_t xh_a = p.xstream ? wbase + stage_w + cl * XTILE : xaddr + c * XTILE;
-                  const uint32_t xl_a = p.xstream ? wbase + stage_w + (p.spc + cl) * XTILE : xaddr + (p.NC + c) * XTILE;
+                  const uint32_t xh_a = p.xstream ? wbase + stage_w + cl * XS : xaddr + c * XS;
+                  const uint32_t xl_a = p.xstream ? wbase + stage_w + (p.spc + cl) * XS : xaddr + (p.NC + c) * XS;
                   const uint64_t bh = desc_k_sw128(xh_a);
                   const uint64_t ah = desc_k_sw128(wbase + cl * parts * WTILE);
 #pragma unroll
-                  for (int kk = 0; kk < 4; ++kk) mma_bf16_ss(d, ah + 2 * kk, bh + 2 * kk, idesc, (c | kk) != 0);
+                  for (int kk = 0; kk < 4; ++kk) {
+                    if constexpr (PAIR)
+                      mma_bf16_ss_pair(d, ah + 2 * kk, bh + 2 * kk, idesc, (c | kk) != 0);
+                    else
+                      mma_bf16_ss(d, ah + 2 * kk, bh + 2 * kk, idesc, (c | kk) != 0);
+                  }
                   if (parts == 2) {
                     const uint64_t bl = desc_k_sw128(xl_a);
                     const uint64_t al = desc_k_sw128(wbase + (cl * parts + 1) * WTILE);
 #pragma unroll
-                    for (int kk = 0; kk < 4; ++kk) mma_bf16_ss(d, ah + 2 * kk, bl + 2 * kk, idesc, 1);
+                    for (int kk = 0; kk < 4; ++kk) {
+                      if constexpr (PAIR)
+                        mma_bf16_ss_pair(d, ah + 2 * kk, bl + 2 * kk, idesc, 1);
+                      else
+                        mma_bf16_ss(d, ah + 2 * kk, bl + 2 * kk, idesc, 1);
+                    }
 #pragma unroll
-                    for (int kk = 0; kk < 4; ++kk) mma_bf16_ss(d, al + 2 * kk, bh + 2 * kk, idesc, 1);
+                    for (int kk = 0; kk < 4; ++kk) {
+                      if constexpr (PAIR)
+                        mma_bf16_ss_pair(d, al + 2 * kk, bh + 2 * kk, idesc, 1);
+                      else
+                        mma_bf16_ss(d, al + 2 * kk, bh + 2 * kk, idesc, 1);
+                    }
                   }
-                  if (t == 8 && !p.xstream) mma_commit(&x_empty[c]);  // chunk c of this band fully consumed
+                  if (t == 8 && !p.xstream) {  // chunk c of this band fully consumed
+                    if constexpr (PAIR)
+                      mma_commit_pair(&x_empty[c], 0x3);
+                    else
+                      mma_commit(&x_empty[c]);
+                  }
                 }
                 if ((p.ablate == 2 || p.ablate == 3) && !p.xstream) {
                   if (t == 8)
-                    for (int cl = 0; cl < p.spc; ++cl) mma_commit(&x_empty[sp * p.spc + cl]);
+                    for (int cl = 0; cl < p.spc; ++cl) {
+                      if constexpr (PAIR)
+                        mma_commit_pair(&x_empty[sp * p.spc + cl], 0x3);
+                      else
+                        mma_commit(&x_empty[sp * p.spc + cl]);
+                    }
                 }
-                mma_commit(&w_empty[wr.s]);
-                if (sp == stages_per_tap - 1) mma_commit(&d_full[db]);
+                if constexpr (PAIR) {
+                  mma_commit_pair(&w_empty[wr.s], 0x3);
+                  if (sp == stages_per_tap - 1) mma_commit_pair(&d_full[db], 0x3);
+                } else {
+                  mma_commit(&w_empty[wr.s]);
+                  if (sp == stages_per_tap - 1) mma_commit(&d_full[db]);
+                }
               }
               __syncwarp();
               wr.adv(S);
@@ -513,11 +640,16 @@ __global__ void __launch_bounds__(THREADS, 1) ri_tc_kernel(const __grid_constant
   } else if (warp >= EPI_WARP0) {
     // ------------------------------------------------------------ epilogue
     asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(REGS_EPILOGUE));
-    epilogue<TW, RPB, CONV>(p, tmem, d_full, d_empty);
+    epilogue<TW, RPB, CONV, PAIR>(p, tmem, d_full, d_empty);
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == 1) tmem_dealloc<512>(tmem);
+  if constexpr (PAIR) {
+    cluster_sync_all();  // no remote arrive / pair MMA may target a CTA that has left
+    if (warp == 1) tmem_dealloc2<512>(tmem);
+  } else {
+    if (warp == 1) tmem_dealloc<512>(tmem);
+  }
 }
 
 // ---- packing kernels ------------------------------------------------------------------
@@ -615,17 +747,22 @@ struct SmemPlan {
 // plus the largest W stage (chunks per stage dividing NC) that leaves >= 2 stages.  When the
 // band does not fit (large Cin), X chunks are streamed with the W stages instead (X re-read
 // from L2 once per tap).
-SmemPlan smem_plan(const TcGeom& g, int parts) {
+SmemPlan smem_plan(const TcGeom& g, int parts, bool pair = false) {
   SmemPlan sp{0, 0, 0, 0};
   const size_t cap = 232448 - 1024 - 1024;  // dynamic smem minus alignment slack / statics
-  const size_t xbuf = (size_t)parts * g.NC * g.xtile;
+  const size_t xt = pair ? g.xtile / 2 : g.xtile;  // a CTA of a pair holds half of every band tile
+  const size_t xbuf = (size_t)parts * g.NC * xt;
   const size_t chunk = (size_t)parts * WTILE;
+  // fewest stages wanted in the W ring: a pair's leader waits on the peer's forwarded
+  // "stage landed" event too, so it needs a deeper prefetch
+  const char* ms = getenv("RC_TC_MIN_STAGES");
+  const size_t min_stages = ms ? (size_t)atoi(ms) : 2;
   if (g.NC <= MAX_NC && xbuf < cap) {
     const size_t budget = cap - xbuf;
     for (int c = g.NC; c >= 1; --c) {
       if (g.NC % c) continue;
       const size_t sb = c * chunk;
-      if (2 * sb <= budget) {
+      if (min_stages * sb <= budget || (c == 1 && 2 * sb <= budget)) {
         sp.spc = c;
         sp.stages = (int)(budget / sb) > 8 ? 8 : (int)(budget / sb);
         sp.bytes = xbuf + sp.stages * sb + 1024;
@@ -633,7 +770,7 @@ SmemPlan smem_plan(const TcGeom& g, int parts) {
       }
     }
   }
-  const size_t schunk = (size_t)parts * (WTILE + g.xtile);
+  const size_t schunk = (size_t)parts * (WTILE + xt);
   for (int c = g.NC; c >= 1; --c) {
     if (g.NC % c) continue;
     const size_t sb = c * schunk;
@@ -708,7 +845,13 @@ int launch_tc(const rc_desc& d, const float* x, const void* bank, const float* b
   RC_CUDA(cudaGetLastError());
   const BankLayout L = bank_layout(d);
   const uint8_t* tcb = static_cast<const uint8_t*>(bank) + L.tc_off;
-  const SmemPlan plan = smem_plan(g, parts);
+  // CTA pairs (cta_group::2) for the N = 96 band of 16-wide images: bit-exact, but measured
+  // SLOWER than single CTAs on C3 (2.75 vs 2.28 ms bf16x3, profiles/r01/pair_ablation.txt):
+  // the pair's load/forward/release chain costs more than the halved B-operand traffic
+  // saves.  Kept behind RC_TC_PAIR=1 for experiments; off by default.
+  const char* pe = getenv("RC_TC_PAIR");
+  const bool pair = d.w == 16 && g.NCT % 2 == 0 && pe && pe[0] == '1';
+  const SmemPlan plan = smem_plan(g, parts, pair);
   TcParams p;
   p.xh = xh;
   p.xl = xl;
@@ -741,14 +884,42 @@ int launch_tc(const rc_desc& d, const float* x, const void* bank, const float* b
   int dev, sms;
   RC_CUDA(cudaGetDevice(&dev));
   RC_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-  const int grid = p.items < sms ? p.items : sms;
-  // [width][single][convention]
+  // [geometry][single][convention]
   static void (*const kernels[3][2][2])(TcParams) = {
-      {{ri_tc_kernel<16, 4, 0>, ri_tc_kernel<16, 4, 1>}, {ri_tc_kernel<16, 1, 0>, ri_tc_kernel<16, 1, 1>}},
-      {{ri_tc_kernel<32, 4, 0>, ri_tc_kernel<32, 4, 1>}, {ri_tc_kernel<32, 1, 0>, ri_tc_kernel<32, 1, 1>}},
-      {{ri_tc_kernel<0, 4, 0>, ri_tc_kernel<0, 4, 1>}, {ri_tc_kernel<0, 1, 0>, ri_tc_kernel<0, 1, 1>}}};
-  void (*fn)(TcParams) = kernels[gi][d.group == RC_GROUP_SINGLE][d.convention == RC_CONV_RAW];
+      {{ri_tc_kernel<16, 4, 0, false>, ri_tc_kernel<16, 4, 1, false>},
+       {ri_tc_kernel<16, 1, 0, false>, ri_tc_kernel<16, 1, 1, false>}},
+      {{ri_tc_kernel<32, 4, 0, false>, ri_tc_kernel<32, 4, 1, false>},
+       {ri_tc_kernel<32, 1, 0, false>, ri_tc_kernel<32, 1, 1, false>}},
+      {{ri_tc_kernel<0, 4, 0, false>, ri_tc_kernel<0, 4, 1, false>},
+       {ri_tc_kernel<0, 1, 0, false>, ri_tc_kernel<0, 1, 1, false>}}};
+  static void (*const pair_kernels[2][2])(TcParams) = {
+      {ri_tc_kernel<16, 4, 0, true>, ri_tc_kernel<16, 4, 1, true>},
+      {ri_tc_kernel<16, 1, 0, true>, ri_tc_kernel<16, 1, 1, true>}};
+  const int single = d.group == RC_GROUP_SINGLE, raw = d.convention == RC_CONV_RAW;
+  void (*fn)(TcParams) = pair ? pair_kernels[single][raw] : kernels[gi][single][raw];
   RC_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)plan.bytes));
+  if (pair) {
+    const int pairs = p.items / 2;  // pair items = N * NCT / 2
+    const int clusters = pairs < sms / 2 ? pairs : sms / 2;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(2 * clusters);
+    cfg.blockDim = dim3(THREADS);
+    cfg.dynamicSmemBytes = plan.bytes;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    prof_begin(s);
+    RC_CUDA(cudaLaunchKernelEx(&cfg, fn, p));
+    prof_end(s);
+    RC_CUDA(cudaGetLastError());
+    return RC_OK;
+  }
+  const int grid = p.items < sms ? p.items : sms;
   prof_begin(s);
   fn<<<grid, THREADS, plan.bytes, s>>>(p);
   prof_end(s);
