@@ -45,17 +45,23 @@ using namespace tc;
 //   TW = 0  : strip of 4 rows x 16 columns of a wider image (W % 16 == 0, W >= 48) from
 //             6 input rows x 18 columns incl. the halo columns           (N = 112, 108 used)
 // RS is the TMEM / operand row stride (pixels per input row of the band).
+//   TW = 8, 4 (H == W): small images, whole images per band and no halo rows at all (the
+//             window rows outside an image are the zero padding): 1 image of 8x8 or 4
+//             images of 4x4 per band (N = 64); a thread owns TR = 16/W full rows.
 template <int TW>
 struct Geo {
   static constexpr bool STRIP = TW == 0;
-  static constexpr int OUT_ROWS = STRIP ? 4 : 64 / TW;      // 4 | 2 | 4
-  static constexpr int IN_ROWS = OUT_ROWS + 2;              // 6 | 4 | 6
-  static constexpr int RS = STRIP ? 18 : TW;                // 16 | 32 | 18
-  static constexpr int BAND_PX = IN_ROWS * RS;              // 96 | 128 | 108
-  static constexpr int MMA_N = (BAND_PX + 15) / 16 * 16;    // 96 | 128 | 112
-  static constexpr int XTILE = MMA_N * 64 * 2;              // bytes of one [MMA_N x 64 ci] bf16 tile
-  static constexpr int HALVES = STRIP ? 1 : TW / 16;        // epilogue threads per output row
-  static constexpr int NDB = MMA_N * 4 + 16 <= 512 ? 4 : 3; // TMEM D buffers
+  static constexpr bool SMALL = TW == 4 || TW == 8;
+  static constexpr int OUT_ROWS = STRIP ? 4 : (SMALL ? 64 / TW : 64 / TW);  // 4 | 2 | 4 | 8 | 16
+  static constexpr int IN_ROWS = SMALL ? OUT_ROWS : OUT_ROWS + 2;
+  static constexpr int RS = STRIP ? 18 : TW;                  // pixels per band row
+  static constexpr int BAND_PX = IN_ROWS * RS;                // 96 | 128 | 108 | 64 | 64
+  static constexpr int MMA_N = (BAND_PX + 15) / 16 * 16;
+  static constexpr int XTILE = MMA_N * 64 * 2;                // bytes of one [MMA_N x 64 ci] bf16 tile
+  static constexpr int HALVES = (STRIP || SMALL) ? 1 : TW / 16;  // epilogue threads per output row
+  static constexpr int NDB = MMA_N * 4 + 16 <= 512 ? 4 : 3;   // TMEM D buffers
+  static constexpr int TR = SMALL ? 16 / TW : 1;              // output rows per epilogue thread
+  static constexpr int IMGS = SMALL ? 64 / (TW * TW) : 1;     // images per band
 };
 constexpr int KC = 64;                  // ci per chunk (one 128-byte swizzle row of bf16)
 constexpr int WTILE = 128 * KC * 2;      // 16 KB
@@ -264,12 +270,57 @@ __device__ __forceinline__ void load_row(uint32_t a, int half, float (&z)[18]) {
   }
 }
 
+// small images: window row I (input row o0 - 1 + I) feeds output row i of the thread's TR
+// rows when I == i + 1 + di; z[c] = input column c - 1 (z[0], z[TW+1] are the zero edges).
+template <int TW, int RPB, int CONV, int T, int I>
+__device__ __forceinline__ void scatter_small(float (&Y)[RPB][XH], const float (&z)[10]) {
+  constexpr int TR = Geo<TW>::TR;
+#pragma unroll
+  for (int r = 0; r < RPB; ++r) {
+    const int di = make_k3(CONV).di[r][T];
+    const int dj = make_k3(CONV).dj[r][T];
+#pragma unroll
+    for (int i = 0; i < TR; ++i) {
+      if (I != i + 1 + di) continue;
+#pragma unroll
+      for (int j = 0; j < TW; ++j) {
+        const int src = j + 1 + dj;
+        if (src < 1 || src > TW) continue;
+        Y[r][i * TW + j] += z[src];
+      }
+    }
+  }
+}
+
+__device__ __forceinline__ void tmem_ld4(uint32_t taddr, float* v) {
+  uint32_t r[4];
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0,%1,%2,%3}, [%4];\n"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+               : "r"(taddr));
+#pragma unroll
+  for (int i = 0; i < 4; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+template <int TW, int RPB, int CONV, int T, int I>
+__device__ __forceinline__ void small_row(uint32_t a, int o0, float (&Y)[RPB][XH]) {
+  const int row = o0 - 1 + I;  // image row of window row I
+  if (row < 0 || row >= TW) return;  // the zero padding (warp-uniform)
+  float z[10];
+  if constexpr (TW == 8)
+    tmem_ld8(a + (I - 1) * TW, z + 1);
+  else
+    tmem_ld4(a + (I - 1) * TW, z + 1);
+  tmem_wait_ld();
+  scatter_small<TW, RPB, CONV, T, I>(Y, z);
+}
+
 struct EpiState {
   uint32_t row_base;  // TMEM address of D-buffer 0, first input row of the thread, its columns
   int db;
   uint32_t dph;
   int lane, half;
   uint32_t dempty_cl;  // CTA pairs: shared::cluster address of the leader's d_empty[0]
+  int o0;              // small images: first output row of the thread (within its image)
 };
 
 // one tap (compile-time T): three single-row TMEM round trips, D released after the last
@@ -283,6 +334,28 @@ __device__ __forceinline__ void epi_tap(EpiState& e, float (&Y)[RPB][XH], uint64
   else
     mbar_wait(&d_full[e.db], e.dph);
   tc_fence_after();
+  if constexpr (Geo<TW>::SMALL) {
+    constexpr int TR = Geo<TW>::TR;
+    small_row<TW, RPB, CONV, T, 0>(a, e.o0, Y);
+    small_row<TW, RPB, CONV, T, 1>(a, e.o0, Y);
+    if constexpr (TR >= 2) small_row<TW, RPB, CONV, T, 2>(a, e.o0, Y);
+    if constexpr (TR >= 2) small_row<TW, RPB, CONV, T, 3>(a, e.o0, Y);
+    if constexpr (TR >= 4) small_row<TW, RPB, CONV, T, 4>(a, e.o0, Y);
+    if constexpr (TR >= 4) small_row<TW, RPB, CONV, T, 5>(a, e.o0, Y);
+    tc_fence_before();
+    __syncwarp();
+    if (e.lane == 0) {
+      if constexpr (PAIR)
+        mbar_arrive_cluster(e.dempty_cl + e.db * 8);
+      else
+        mbar_arrive(&d_empty[e.db]);
+    }
+    if (++e.db == NDB) {
+      e.db = 0;
+      e.dph ^= 1;
+    }
+    return;
+  }
   load_row<TW>(a, e.half, z);
   scatter_row<TW, RPB, CONV, T, 0>(Y, z);
   load_row<TW>(a + Geo<TW>::RS, e.half, z);
@@ -328,8 +401,12 @@ __device__ void epilogue(const TcParams& p, uint32_t tmem, uint64_t* d_full, uin
   const int sub = (warp - EPI_WARP0) / 4;
   const int srow = sub / G::HALVES, half = sub % G::HALVES;
   const int co_l = q * 32 + lane;
-  EpiState e{tmem + ((uint32_t)(q * 32) << 16) + D0 + srow * G::RS + half * 16, 0, 0, lane, half,
-             PAIR ? mapa_shared(d_empty, 0) : 0u};
+  // small images: sub = image of the band (4x4) or row pair (8x8); row_base -> its first row
+  const int s_img = G::SMALL ? (G::IMGS > 1 ? sub : 0) : 0;
+  const int o0 = G::SMALL ? (G::IMGS > 1 ? 0 : sub * G::TR) : 0;
+  const uint32_t rb = G::SMALL ? (uint32_t)((s_img * TW + o0) * G::RS) : (uint32_t)(srow * G::RS + half * 16);
+  EpiState e{tmem + ((uint32_t)(q * 32) << 16) + D0 + rb, 0, 0, lane, half,
+             PAIR ? mapa_shared(d_empty, 0) : 0u, o0};
   const int nstrip = G::STRIP ? p.W / 16 : 1;
   float Y[RPB][XH];
   const Work wk = make_work<PAIR>(p);
@@ -368,9 +445,10 @@ __device__ void epilogue(const TcParams& p, uint32_t tmem, uint64_t* d_full, uin
         epi_tap<TW, RPB, CONV, 6, PAIR>(e, Y, d_full, d_empty);
         epi_tap<TW, RPB, CONV, 7, PAIR>(e, Y, d_full, d_empty);
         epi_tap<TW, RPB, CONV, 8, PAIR>(e, Y, d_full, d_empty);
-        const int row = G::OUT_ROWS * (k / nstrip) + srow;
-        const int x0 = (k % nstrip) * 16 + half * 16;
-        if (n < p.N && co < p.Cout && row < p.H && p.ablate != 1) finalize_row<TW, RPB>(p, Y, n, co, b, row, x0);
+        const int row = G::SMALL ? o0 : G::OUT_ROWS * (k / nstrip) + srow;
+        const int x0 = G::SMALL ? 0 : (k % nstrip) * 16 + half * 16;
+        const int img = G::SMALL ? n * G::IMGS + s_img : n;  // small: n indexes bands of IMGS images
+        if (img < p.N && co < p.Cout && row < p.H && p.ablate != 1) finalize_row<TW, RPB>(p, Y, img, co, b, row, x0);
       }
   }
 }
@@ -664,7 +742,7 @@ __device__ __forceinline__ void split_bf16(float v, __nv_bfloat16& hi, __nv_bflo
 // MMA_N - BAND_PX filler pixels are zero.
 template <int TW>
 __global__ void x_pack_kernel(const float* __restrict__ x, uint8_t* __restrict__ xh,
-                              uint8_t* __restrict__ xl, int Cin, int H, int W, int NBK, int NC) {
+                              uint8_t* __restrict__ xl, int Cin, int H, int W, int NBK, int NC, int Nimg) {
   using G = Geo<TW>;
   __shared__ float tile[KC][G::MMA_N + 1];
   const int c = blockIdx.x, bk = blockIdx.y, n = blockIdx.z;
@@ -672,10 +750,18 @@ __global__ void x_pack_kernel(const float* __restrict__ x, uint8_t* __restrict__
   const int k = bk / nstrip, j = bk % nstrip;
   for (int i = threadIdx.x; i < KC * G::MMA_N; i += blockDim.x) {
     const int cl = i / G::MMA_N, px = i % G::MMA_N;
-    const int ci = c * KC + cl, row = k * G::OUT_ROWS - 1 + px / G::RS;
-    const int col = G::STRIP ? j * 16 - 1 + px % G::RS : px % G::RS;
-    const bool in = px < G::BAND_PX && ci < Cin && row >= 0 && row < H && col >= 0 && col < W;
-    tile[cl][px] = in ? x[(((size_t)n * Cin + ci) * H + row) * W + col] : 0.f;
+    const int ci = c * KC + cl;
+    int img = n, row, col;
+    if constexpr (G::SMALL) {  // band = IMGS whole images, px = (image, row, col), no halo rows
+      img = n * G::IMGS + px / (TW * TW);
+      row = (px / TW) % TW;
+      col = px % TW;
+    } else {
+      row = k * G::OUT_ROWS - 1 + px / G::RS;
+      col = G::STRIP ? j * 16 - 1 + px % G::RS : px % G::RS;
+    }
+    const bool in = px < G::BAND_PX && ci < Cin && img < Nimg && row >= 0 && row < H && col >= 0 && col < W;
+    tile[cl][px] = in ? x[(((size_t)img * Cin + ci) * H + row) * W + col] : 0.f;
   }
   __syncthreads();
   const size_t tidx = ((size_t)n * NBK + bk) * NC + c;
@@ -724,17 +810,22 @@ __global__ void w_pack_kernel(const float* __restrict__ bases, uint8_t* __restri
 }
 
 struct TcGeom {
+  int gi;       // geometry: 0 = TW 16, 1 = TW 32, 2 = strips, 3 = 8x8 images, 4 = 4x4 images
+  int units;    // band owners: images, or bands of IMGS small images
   int NBK, NC, NCT, xtile;
   size_t x_plane, w_plane;
 };
 TcGeom geom(const rc_desc& d) {
   TcGeom g;
-  const int out_rows = d.w == 32 ? Geo<32>::OUT_ROWS : (d.w == 16 ? Geo<16>::OUT_ROWS : Geo<0>::OUT_ROWS);
-  g.xtile = d.w == 32 ? Geo<32>::XTILE : (d.w == 16 ? Geo<16>::XTILE : Geo<0>::XTILE);
-  g.NBK = (d.h + out_rows - 1) / out_rows * (d.w == 16 || d.w == 32 ? 1 : d.w / 16);
+  g.gi = d.w == 16 ? 0 : d.w == 32 ? 1 : (d.w == 8 && d.h == 8) ? 3 : (d.w == 4 && d.h == 4) ? 4 : 2;
+  static const int out_rows_of[5] = {Geo<16>::OUT_ROWS, Geo<32>::OUT_ROWS, Geo<0>::OUT_ROWS, 8, 4};
+  static const int xtile_of[5] = {Geo<16>::XTILE, Geo<32>::XTILE, Geo<0>::XTILE, Geo<8>::XTILE, Geo<4>::XTILE};
+  g.xtile = xtile_of[g.gi];
+  g.units = g.gi == 3 ? d.n : (g.gi == 4 ? (d.n + 3) / 4 : d.n);
+  g.NBK = g.gi >= 3 ? 1 : (d.h + out_rows_of[g.gi] - 1) / out_rows_of[g.gi] * (g.gi == 2 ? d.w / 16 : 1);
   g.NC = (d.c_in + KC - 1) / KC;
   g.NCT = (d.c_out + 127) / 128;
-  g.x_plane = (size_t)d.n * g.NBK * g.NC * g.xtile;
+  g.x_plane = (size_t)g.units * g.NBK * g.NC * g.xtile;
   g.w_plane = (size_t)num_bases(d) * g.NCT * 9 * g.NC * WTILE;
   return g;
 }
@@ -792,7 +883,9 @@ bool tc_supported(const rc_desc& d) {
   const int R = d.orientations;
   const bool fold_ok = d.pool == RC_POOL_NONE || (d.pool == RC_POOL_AVG && (R & (R - 1)) == 0) || gf == 1 ||
                        gf == 2 || gf % 4 == 0;
-  if (!(d.k == 3 && (d.w == 16 || d.w == 32 || (d.w >= 48 && d.w % 16 == 0)) && fold_ok &&
+  const bool geom_ok = d.w == 16 || d.w == 32 || (d.w >= 48 && d.w % 16 == 0) || (d.w == 8 && d.h == 8) ||
+                       (d.w == 4 && d.h == 4);
+  if (!(d.k == 3 && geom_ok && fold_ok &&
         (d.precision == RC_PREC_BF16 || d.precision == RC_PREC_BF16X3 || d.precision == RC_PREC_AUTO)))
     return false;
   const int parts = d.precision == RC_PREC_BF16 ? 1 : 2;
@@ -822,10 +915,12 @@ int launch_tc(const rc_desc& d, const float* x, const void* bank, const float* b
               void* ws, size_t ws_bytes, cudaStream_t s, bool dry_run, const char** name) {
   if (!tc_supported(d)) return RC_ERR_UNSUPPORTED;
   if (name) {
-    static const char* names[3][2] = {{"tc_k3w16_bf16x3", "tc_k3w16_bf16"},
+    static const char* names[5][2] = {{"tc_k3w16_bf16x3", "tc_k3w16_bf16"},
                                       {"tc_k3w32_bf16x3", "tc_k3w32_bf16"},
-                                      {"tc_k3strip_bf16x3", "tc_k3strip_bf16"}};
-    *name = names[d.w == 16 ? 0 : (d.w == 32 ? 1 : 2)][d.precision == RC_PREC_BF16];
+                                      {"tc_k3strip_bf16x3", "tc_k3strip_bf16"},
+                                      {"tc_k3img8_bf16x3", "tc_k3img8_bf16"},
+                                      {"tc_k3img4_bf16x3", "tc_k3img4_bf16"}};
+    *name = names[geom(d).gi][d.precision == RC_PREC_BF16];
   }
   if (dry_run || d.n == 0) return RC_OK;
   const TcGeom g = geom(d);
@@ -835,13 +930,15 @@ int launch_tc(const rc_desc& d, const float* x, const void* bank, const float* b
   const int parts = passes == 3 ? 2 : 1;
   uint8_t* xh = static_cast<uint8_t*>(ws);
   uint8_t* xl = passes == 3 ? xh + g.x_plane : nullptr;
-  const int gi = d.w == 16 ? 0 : (d.w == 32 ? 1 : 2);
-  if (gi == 1)
-    x_pack_kernel<32><<<dim3(g.NC, g.NBK, d.n), 256, 0, s>>>(x, xh, xl, d.c_in, d.h, d.w, g.NBK, g.NC);
-  else if (gi == 0)
-    x_pack_kernel<16><<<dim3(g.NC, g.NBK, d.n), 256, 0, s>>>(x, xh, xl, d.c_in, d.h, d.w, g.NBK, g.NC);
-  else
-    x_pack_kernel<0><<<dim3(g.NC, g.NBK, d.n), 256, 0, s>>>(x, xh, xl, d.c_in, d.h, d.w, g.NBK, g.NC);
+  const int gi = g.gi;
+  const dim3 pgrid(g.NC, g.NBK, g.units);
+  switch (gi) {
+    case 0: x_pack_kernel<16><<<pgrid, 256, 0, s>>>(x, xh, xl, d.c_in, d.h, d.w, g.NBK, g.NC, d.n); break;
+    case 1: x_pack_kernel<32><<<pgrid, 256, 0, s>>>(x, xh, xl, d.c_in, d.h, d.w, g.NBK, g.NC, d.n); break;
+    case 2: x_pack_kernel<0><<<pgrid, 256, 0, s>>>(x, xh, xl, d.c_in, d.h, d.w, g.NBK, g.NC, d.n); break;
+    case 3: x_pack_kernel<8><<<pgrid, 256, 0, s>>>(x, xh, xl, d.c_in, d.h, d.w, g.NBK, g.NC, d.n); break;
+    default: x_pack_kernel<4><<<pgrid, 256, 0, s>>>(x, xh, xl, d.c_in, d.h, d.w, g.NBK, g.NC, d.n); break;
+  }
   RC_CUDA(cudaGetLastError());
   const BankLayout L = bank_layout(d);
   const uint8_t* tcb = static_cast<const uint8_t*>(bank) + L.tc_off;
@@ -876,7 +973,7 @@ int launch_tc(const rc_desc& d, const float* x, const void* bank, const float* b
   p.w_stages = plan.stages;
   p.spc = plan.spc;
   p.xstream = plan.xstream;
-  p.items = g.NCT * d.n;
+  p.items = g.NCT * g.units;
   {
     const char* ab = getenv("RC_TC_ABLATE");  // profiling switch, see TcParams::ablate
     p.ablate = ab ? atoi(ab) : 0;
@@ -885,13 +982,17 @@ int launch_tc(const rc_desc& d, const float* x, const void* bank, const float* b
   RC_CUDA(cudaGetDevice(&dev));
   RC_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
   // [geometry][single][convention]
-  static void (*const kernels[3][2][2])(TcParams) = {
+  static void (*const kernels[5][2][2])(TcParams) = {
       {{ri_tc_kernel<16, 4, 0, false>, ri_tc_kernel<16, 4, 1, false>},
        {ri_tc_kernel<16, 1, 0, false>, ri_tc_kernel<16, 1, 1, false>}},
       {{ri_tc_kernel<32, 4, 0, false>, ri_tc_kernel<32, 4, 1, false>},
        {ri_tc_kernel<32, 1, 0, false>, ri_tc_kernel<32, 1, 1, false>}},
       {{ri_tc_kernel<0, 4, 0, false>, ri_tc_kernel<0, 4, 1, false>},
-       {ri_tc_kernel<0, 1, 0, false>, ri_tc_kernel<0, 1, 1, false>}}};
+       {ri_tc_kernel<0, 1, 0, false>, ri_tc_kernel<0, 1, 1, false>}},
+      {{ri_tc_kernel<8, 4, 0, false>, ri_tc_kernel<8, 4, 1, false>},
+       {ri_tc_kernel<8, 1, 0, false>, ri_tc_kernel<8, 1, 1, false>}},
+      {{ri_tc_kernel<4, 4, 0, false>, ri_tc_kernel<4, 4, 1, false>},
+       {ri_tc_kernel<4, 1, 0, false>, ri_tc_kernel<4, 1, 1, false>}}};
   static void (*const pair_kernels[2][2])(TcParams) = {
       {ri_tc_kernel<16, 4, 0, true>, ri_tc_kernel<16, 4, 1, true>},
       {ri_tc_kernel<16, 1, 0, true>, ri_tc_kernel<16, 1, 1, true>}};

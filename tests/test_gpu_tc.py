@@ -213,6 +213,39 @@ def test_tc_large_cin_streamed_x(O, dev, cfg, precision):
         assert np.array_equal(a, a_ref)
 
 
+SMALL_CONFIGS = [
+    # (n, cin, s, cout, group, R, pool, g, convention): whole 8x8 / 4x4 images per band
+    (32, 64, 8, 256, "single", 1, "none", 1, "scatter"),      # C1 shape
+    (3, 16, 8, 130, "p4m", 8, "subgroup", 4, "raw"),
+    (5, 32, 4, 256, "single", 1, "none", 1, "scatter"),       # ragged group of 4 images
+    (6, 64, 4, 128, "p4", 4, "max", 4, "scatter"),
+    (2, 100, 8, 128, "steer", 8, "avg", 4, "scatter"),
+]
+
+
+@pytest.mark.parametrize("precision", ["bf16", "bf16x3"])
+@pytest.mark.parametrize("cfg", SMALL_CONFIGS, ids=lambda c: "-".join(map(str, c)))
+def test_tc_small_images(O, dev, cfg, precision):
+    import paper_2512_08888_b200 as P
+    n, cin, sz, cout, g, R, pool, pg, conv = cfg
+    d = O.Desc(n, cin, sz, sz, cout, 3, g, R, pool, pg, conv)
+    rng = np.random.default_rng(abs(hash(cfg)) % 2**32)
+    x = dyadic(rng, (n, cin, sz, sz))
+    w0 = dyadic(rng, (cout, cin, 3, 3))
+    w1 = dyadic(rng, (cout, cin, 3, 3)) if g == "steer" else None
+    bias = dyadic(rng, cout)
+    y_ref, a_ref = O.ri_forward(d, x, w0, w1, bias)
+    y, a = run(P, d, x, w0, w1, bias, precision, dev)
+    y = y.reshape(y_ref.shape)
+    if g == "steer":
+        err = np.abs(y.astype(np.float64) - y_ref).max() / np.abs(y_ref).max()
+        assert err <= TOL[precision], err
+        return
+    assert np.array_equal(y, y_ref), f"max|dy| = {np.abs(y - y_ref).max()}"
+    if a_ref is not None and g != "single":
+        assert np.array_equal(a, a_ref), f"argmax mismatches {(a != a_ref).sum()}"
+
+
 @pytest.mark.parametrize("kernel", ["tc", "simt"])
 def test_fused_relu_activation(O, dev, kernel):
     """activation = relu is applied after the bias (relu of the oracle's pooled output)."""
