@@ -430,8 +430,8 @@ __device__ void epilogue(const TcParams& p, uint32_t tmem, uint64_t* d_full, uin
       }
       continue;
     }
-    for (int b = 0; b < p.NB; ++b)
-      for (int k = 0; k < p.NBK; ++k) {
+    for (int k = 0; k < p.NBK; ++k)
+      for (int b = 0; b < p.NB; ++b) {
 #pragma unroll
         for (int r = 0; r < RPB; ++r)
 #pragma unroll
@@ -538,12 +538,12 @@ __global__ void __launch_bounds__(THREADS, 1) ri_tc_kernel(const __grid_constant
     uint32_t xc = 0;  // bands loaded so far (phase of the per-chunk X barriers)
     for (int item = wk.first; item < wk.count; item += wk.stride) {
       const int n = wk.n(item), ct = wk.ct(item);
-      for (int b = 0; b < p.NB; ++b)
-        for (int k = 0; k < p.NBK; ++k) {
+      for (int k = 0; k < p.NBK; ++k)
+        for (int b = 0; b < p.NB; ++b) {
           const size_t tile = ((size_t)n * p.NBK + k) * p.NC;
           const uint8_t* wsrc = p.w + (((size_t)b * p.NCT + ct) * 9) * p.NC * parts * WTILE;
           for (int st = 0; st < 9 * stages_per_tap; ++st) {
-            if (!p.xstream && st < stages_per_tap) {  // tap 0: this stage's X chunks of the new band first
+            if (!p.xstream && b == 0 && st < stages_per_tap) {  // new band, tap 0: its X chunks first
               for (int cl = 0; cl < p.spc; ++cl) {
                 const int c = st * p.spc + cl;
                 if (xc > 0) {
@@ -587,7 +587,7 @@ __global__ void __launch_bounds__(THREADS, 1) ri_tc_kernel(const __grid_constant
             __syncwarp();
             wr.adv(S);
           }
-          ++xc;
+          if (b == p.NB - 1) ++xc;  // the band's X is reloaded only after its last base
         }
     }
   } else if (warp == 1 && PAIR && rank != 0) {
@@ -597,11 +597,11 @@ __global__ void __launch_bounds__(THREADS, 1) ri_tc_kernel(const __grid_constant
     Ring wr;
     uint32_t xc = 0;
     for (int item = wk.first; item < wk.count; item += wk.stride)
-      for (int b = 0; b < p.NB; ++b)
-        for (int k = 0; k < p.NBK; ++k) {
+      for (int k = 0; k < p.NBK; ++k)
+        for (int b = 0; b < p.NB; ++b) {
           for (int t = 0; t < 9; ++t)
             for (int sp = 0; sp < stages_per_tap; ++sp) {
-              if (t == 0 && !p.xstream)
+              if (t == 0 && b == 0 && !p.xstream)
                 for (int cl = 0; cl < p.spc; ++cl) {
                   const int c = sp * p.spc + cl;
                   mbar_wait(&x_full[c], xc & 1);
@@ -613,7 +613,7 @@ __global__ void __launch_bounds__(THREADS, 1) ri_tc_kernel(const __grid_constant
               __syncwarp();
               wr.adv(S);
             }
-          ++xc;
+          if (b == p.NB - 1) ++xc;
         }
   } else if (warp == 1) {
     // ------------------------------------------------------------ MMA issuer (whole warp
@@ -625,8 +625,8 @@ __global__ void __launch_bounds__(THREADS, 1) ri_tc_kernel(const __grid_constant
     int db = 0;
     uint32_t dph = 0;
     for (int item = wk.first; item < wk.count; item += wk.stride) {
-      for (int b = 0; b < p.NB; ++b)
-        for (int k = 0; k < p.NBK; ++k) {
+      for (int k = 0; k < p.NBK; ++k)
+        for (int b = 0; b < p.NB; ++b) {
           for (int t = 0; t < 9; ++t) {
             if (gd >= NDB) {
               if constexpr (PAIR)
@@ -637,7 +637,7 @@ __global__ void __launch_bounds__(THREADS, 1) ri_tc_kernel(const __grid_constant
             tc_fence_after();
             const uint32_t d = tmem + D0 + db * G::MMA_N;
             for (int sp = 0; sp < stages_per_tap; ++sp) {
-              if (t == 0 && !p.xstream)
+              if (t == 0 && b == 0 && !p.xstream)
                 for (int cl = 0; cl < p.spc; ++cl) {
                   mbar_wait(&x_full[sp * p.spc + cl], xc & 1);
                   if constexpr (PAIR) mbar_wait_spin(&px_full[sp * p.spc + cl], xc & 1);
@@ -679,7 +679,7 @@ __global__ void __launch_bounds__(THREADS, 1) ri_tc_kernel(const __grid_constant
                         mma_bf16_ss(d, al + 2 * kk, bh + 2 * kk, idesc, 1);
                     }
                   }
-                  if (t == 8 && !p.xstream) {  // chunk c of this band fully consumed
+                  if (t == 8 && b == p.NB - 1 && !p.xstream) {  // chunk c of this band fully consumed
                     if constexpr (PAIR)
                       mma_commit_pair(&x_empty[c], 0x3);
                     else
@@ -687,7 +687,7 @@ __global__ void __launch_bounds__(THREADS, 1) ri_tc_kernel(const __grid_constant
                   }
                 }
                 if ((p.ablate == 2 || p.ablate == 3) && !p.xstream) {
-                  if (t == 8)
+                  if (t == 8 && b == p.NB - 1)
                     for (int cl = 0; cl < p.spc; ++cl) {
                       if constexpr (PAIR)
                         mma_commit_pair(&x_empty[sp * p.spc + cl], 0x3);
@@ -712,7 +712,7 @@ __global__ void __launch_bounds__(THREADS, 1) ri_tc_kernel(const __grid_constant
               dph ^= 1;
             }
           }
-          ++xc;
+          if (b == p.NB - 1) ++xc;
         }
     }
   } else if (warp >= EPI_WARP0) {

@@ -468,3 +468,49 @@ def orientation_pool_max(f: torch.Tensor):
 def subgroup_pool_max(f: torch.Tensor, group_size: int = 4):
     """blockwise max over contiguous blocks, block-local argmax."""
     return _pool(f, "subgroup", group_size)
+
+
+# ------------------------------------------------- steerable regularisers (SPEC:457-514)
+# Training-side scalars over the B filter pairs of a basis (SURVEY §8 f4): tiny reductions
+# over the weights, computed with torch ops wherever the basis lives.  Not on the forward
+# hot path.
+def gaussian_derivative_basis(k: int, sigma: float, out_channels: int = 1, in_channels: int = 1,
+                              device="cpu", dtype=torch.float64) -> SteerableBasis:
+    """f_x ~ -x exp(-(x^2+y^2)/2s^2), f_y ~ -y exp(..), unit L2, centred grid."""
+    if k < 1 or k % 2 == 0:
+        raise ValueError("gaussian_derivative_basis: K must be odd")
+    if sigma <= 0:
+        raise ValueError("gaussian_derivative_basis: sigma must be positive")
+    c = k // 2
+    ax = torch.arange(k, dtype=torch.float64) - c
+    yy, xx = torch.meshgrid(ax, ax, indexing="ij")
+    g = torch.exp(-(xx * xx + yy * yy) / (2 * sigma * sigma))
+    fx, fy = -xx * g, -yy * g
+    fx, fy = fx / fx.norm(), fy / fy.norm()
+    shape = (out_channels, in_channels, k, k)
+    return SteerableBasis(fx.expand(shape).to(device=device, dtype=dtype).contiguous(),
+                          fy.expand(shape).to(device=device, dtype=dtype).contiguous())
+
+
+def loss_mag(basis: SteerableBasis) -> torch.Tensor:
+    """SPEC:457-466 Eq. (19): mean over filters b of (||w_x_b|| - ||w_y_b||)^2."""
+    nx = basis.f_x.reshape(basis.f_x.shape[0], -1).double().norm(dim=1)
+    ny = basis.f_y.reshape(basis.f_y.shape[0], -1).double().norm(dim=1)
+    return ((nx - ny) ** 2).mean()
+
+
+def loss_orth(basis: SteerableBasis, eps: float = 1e-8) -> torch.Tensor:
+    """SPEC:467-474 Eq. (20): mean over b of (<w_x, w_y> / (||w_x|| ||w_y|| + eps))^2."""
+    if eps <= 0:
+        raise ValueError("loss_orth: eps must be positive")
+    x = basis.f_x.reshape(basis.f_x.shape[0], -1).double()
+    y = basis.f_y.reshape(basis.f_y.shape[0], -1).double()
+    c = (x * y).sum(dim=1) / (x.norm(dim=1) * y.norm(dim=1) + eps)
+    return (c ** 2).mean()
+
+
+def total_loss(ce, basis: SteerableBasis, lambda_mag: float, lambda_orth: float, eps: float = 1e-8):
+    """SPEC:475-483 Eq. (18): ce + lambda_mag * L_mag + lambda_orth * L_orth."""
+    if lambda_mag < 0 or lambda_orth < 0:
+        raise ValueError("total_loss: lambdas must be >= 0")
+    return ce + lambda_mag * loss_mag(basis) + lambda_orth * loss_orth(basis, eps)
