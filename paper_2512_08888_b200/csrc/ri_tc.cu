@@ -818,6 +818,13 @@ struct TcGeom {
 TcGeom geom(const rc_desc& d) {
   TcGeom g;
   g.gi = d.w == 16 ? 0 : d.w == 32 ? 1 : (d.w == 8 && d.h == 8) ? 3 : (d.w == 4 && d.h == 4) ? 4 : 2;
+  if (g.gi == 1) {
+    // W = 32 runs as two 4x16 strips per 4 rows (N = 112, 1.69 input px per output px)
+    // rather than 2-row bands (N = 128, 2.0): 5-8% faster on C4 (profiles/r01/strip32.txt).
+    // RC_TC_ROWS32=1 selects the 2-row bands (A/B testing).
+    const char* e = getenv("RC_TC_ROWS32");
+    if (!(e && e[0] == '1')) g.gi = 2;
+  }
   static const int out_rows_of[5] = {Geo<16>::OUT_ROWS, Geo<32>::OUT_ROWS, Geo<0>::OUT_ROWS, 8, 4};
   static const int xtile_of[5] = {Geo<16>::XTILE, Geo<32>::XTILE, Geo<0>::XTILE, Geo<8>::XTILE, Geo<4>::XTILE};
   g.xtile = xtile_of[g.gi];

@@ -56,7 +56,7 @@ def test_stack_c5_shape_graph_and_kernels(O, dev):
     from paper_2512_08888_b200.stack import RIStack, StackSpec
     stack = RIStack(StackSpec(), dev, seed=5)
     ks = stack.kernels(2)
-    assert ks[2].startswith("tc_k3w32") and ks[4].startswith("tc_k3w16"), ks
+    assert ks[2].startswith("tc_k3strip") and ks[4].startswith("tc_k3w16"), ks
     x = torch.rand((2, 3, 64, 64), device=dev) * 2 - 1
     eager = stack.forward(x).clone()
     graph = stack.graph_forward(x).clone()

@@ -104,9 +104,11 @@ TC32_CONFIGS = [
 ]
 
 
+@pytest.mark.parametrize("rows32", ["0", "1"])  # W=32 as 4x16 strips (default) or 2-row bands
 @pytest.mark.parametrize("precision", ["bf16", "bf16x3"])
 @pytest.mark.parametrize("cfg", TC32_CONFIGS, ids=lambda c: "-".join(map(str, c)))
-def test_tc_w32_dyadic_bitexact(O, dev, cfg, precision):
+def test_tc_w32_dyadic_bitexact(O, dev, cfg, precision, rows32, monkeypatch):
+    monkeypatch.setenv("RC_TC_ROWS32", rows32)
     import paper_2512_08888_b200 as P
     n, cin, h, cout, g, R, pool, pg, conv = cfg
     d = O.Desc(n, cin, h, 32, cout, 3, g, R, pool, pg, conv)
