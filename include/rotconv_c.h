@@ -131,6 +131,21 @@ int rc_ri_conv_forward(const rc_desc* d, const float* d_x, const void* d_bank,
  * "tc_bf16x3", "generic"); NULL if none */
 const char* rc_kernel_name(const rc_desc* d);
 
+/* ---- backward (SPEC backward module) -----------------------------
+ * Gradients of the fused layer for an upstream gradient d_gy (N, Cout, R', H, W):
+ *   ReLU backward (needs the forward output d_y; d_gy is MASKED IN PLACE), bias gradient
+ *   (d_dbias, Cout), pool backward through the forward's argmax map (Eq. 11/12) into
+ *   d_scratch (rc_backward_scratch_bytes: the unpooled (N, Cout, R, H, W) gradient),
+ *   input gradient d_dx (N, Cin, H, W) as one single-orientation transposed conv on this
+ *   library's kernels (Eq. 13/15), and parameter gradients (Eq. 14 via im2col + FP32
+ *   cuBLAS SGEMM, Eq. 16 inverse-rotation sum, then the group's chain rule): d_dw0 = dW
+ *   (single/p4/p4m) or d f_x (steer), d_dw1 = d f_y (steer).  Any output may be NULL. */
+size_t rc_backward_scratch_bytes(const rc_desc* d);
+size_t rc_backward_workspace_size(const rc_desc* d);
+int rc_ri_conv_backward(const rc_desc* d, const float* d_x, const void* d_bank, const float* d_y,
+                        float* d_gy, const uint8_t* d_argmax, float* d_dx, float* d_dw0, float* d_dw1,
+                        float* d_dbias, float* d_scratch, void* d_ws, size_t ws_bytes, void* stream);
+
 /* Orientation pooling of an already materialised OrientedFeature batch
  * (N, Cout, R, H, W) -- SPEC:283-309 as standalone ops. */
 int rc_orientation_pool(int n, int c_out, int r, int h, int w, int pool, int pool_group,

@@ -11,6 +11,6 @@ from .rotconv import (  # noqa: F401
     group_conv_scatter_reuse, orientation_pool_avg, orientation_pool_max, ri_conv,
     ri_conv_forward, scatter_conv_multi, scatter_conv_raw_multi, scatter_conv_single,
     shard_range, steer, subgroup_pool_max, tiled_scatter_conv, transform_kernel,
-    gaussian_derivative_basis, loss_mag, loss_orth, total_loss)
+    gaussian_derivative_basis, loss_mag, loss_orth, total_loss, ri_conv_backward, RIConvFunction)
 
 __all__ = [n for n in dir() if not n.startswith("_")]

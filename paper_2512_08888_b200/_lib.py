@@ -53,6 +53,9 @@ SIGNATURES = {
     "rc_orientation_bank_host": (C.c_int, [_D, _VP, _VP, _VP, C.c_int]),
     "rc_orientation_pool_host": (C.c_int, [C.c_int] * 7 + [_VP, _VP, _VP, _VP, C.c_int]),
     "rc_mgpu_forward_host": (C.c_int, [_D, _VP, _VP, _VP, _VP, _VP, _VP, C.c_int, _P(C.c_int)]),
+    "rc_backward_scratch_bytes": (C.c_size_t, [_D]),
+    "rc_backward_workspace_size": (C.c_size_t, [_D]),
+    "rc_ri_conv_backward": (C.c_int, [_D] + [_VP] * 11 + [C.c_size_t, _VP]),
     "rc_maxpool2x2": (C.c_int, [C.c_int] * 4 + [_VP, _VP, _VP]),
     "rc_gap_linear": (C.c_int, [C.c_int] * 4 + [_VP, _VP, _VP, C.c_int, _VP, _VP]),
     "rc_tiled_scatter_conv_host": (C.c_int, [_VP] + [C.c_int] * 3 + [_VP] + [C.c_int] * 9 +

@@ -214,6 +214,13 @@ int dispatch(const rc_desc& d, const float* x, const void* bank, const float* bi
 
 }  // namespace
 
+namespace rc {
+int dispatch_forward(const rc_desc& d, const float* x, const void* bank, const float* bias, float* y,
+                     uint8_t* am, void* ws, size_t ws_bytes, cudaStream_t s) {
+  return dispatch(d, x, bank, bias, y, am, ws, ws_bytes, s, false, nullptr);
+}
+}  // namespace rc
+
 extern "C" {
 
 int rc_abi_version(void) { return RC_ABI_VERSION; }
@@ -320,6 +327,44 @@ int rc_ri_conv_forward(const rc_desc* d, const float* d_x, const void* d_bank,
   if (d->n > 0 && (!d_x || !d_bank || !d_y)) return fail(RC_ERR_INVALID, "ri_conv: null pointer");
   return dispatch(*d, d_x, d_bank, d_bias, d_y, d_argmax, d_ws, ws_bytes, static_cast<cudaStream_t>(stream),
                   false, nullptr);
+}
+
+size_t rc_backward_scratch_bytes(const rc_desc* d) {
+  if (!d || validate(*d) != RC_OK) return 0;
+  return (size_t)d->n * d->c_out * num_bases(*d) * rot_per_base(*d) * d->h * d->w * sizeof(float);
+}
+
+size_t rc_backward_workspace_size(const rc_desc* d) {
+  if (!d || validate(*d) != RC_OK) return 0;
+  const size_t a = bwd_input_ws(*d), b = bwd_weight_ws(*d);
+  return a > b ? a : b;
+}
+
+int rc_ri_conv_backward(const rc_desc* d, const float* d_x, const void* d_bank, const float* d_y, float* d_gy,
+                        const uint8_t* d_argmax, float* d_dx, float* d_dw0, float* d_dw1, float* d_dbias,
+                        float* d_scratch, void* d_ws, size_t ws_bytes, void* stream) {
+  RC_CHECK_DESC(d);
+  if (d->n == 0) return RC_OK;
+  if (!d_gy || !d_bank || !d_scratch) return fail(RC_ERR_INVALID, "ri_conv_backward: null pointer");
+  if ((d->pool == RC_POOL_MAX || d->pool == RC_POOL_SUBGROUP) && !d_argmax)
+    return fail(RC_ERR_INVALID, "pool_backward_max: argmax map required");
+  if (d->activation == RC_ACT_RELU && !d_y) return fail(RC_ERR_INVALID, "ri_conv_backward: relu needs the forward output");
+  if ((d_dw0 || (d_dw1 && d->group == RC_GROUP_STEER)) && !d_x)
+    return fail(RC_ERR_INVALID, "ri_conv_backward: weight gradients need the forward input");
+  if (d->group == RC_GROUP_STEER && d_dw0 && !d_dw1)
+    return fail(RC_ERR_INVALID, "ri_conv_backward: steerable layers need both f_x and f_y gradients");
+  if (ws_bytes < rc_backward_workspace_size(d) || !d_ws)
+    return fail(RC_ERR_WORKSPACE, "ri_conv_backward: workspace too small");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const long long ny = (long long)d->n * d->c_out * out_orientations(*d) * d->h * d->w;
+  int st = RC_OK;
+  if (d->activation == RC_ACT_RELU) st = launch_relu_backward(d_y, d_gy, ny, s);  // d_gy masked in place
+  if (st == RC_OK && d_dbias)
+    st = launch_bias_backward(d_gy, d_dbias, d->n, d->c_out, (long long)out_orientations(*d) * d->h * d->w, s);
+  if (st == RC_OK) st = launch_pool_backward(*d, d_gy, d_argmax, d_scratch, s);
+  if (st == RC_OK && d_dx) st = launch_bwd_input(*d, d_scratch, d_bank, d_dx, d_ws, s);
+  if (st == RC_OK && d_dw0) st = launch_bwd_weight(*d, d_x, d_scratch, d_dw0, d_dw1, d_ws, s);
+  return st;
 }
 
 int rc_orientation_pool(int n, int c_out, int r, int h, int w, int pool, int pool_group,

@@ -77,6 +77,18 @@ int launch_generic(const rc_desc& d, const float* x, const void* bank, const flo
                    float* y, uint8_t* argmax, cudaStream_t s, const char** name);
 int launch_pool(int n, int c_out, int r, int h, int w, int pool, int g, const float* f,
                 const float* bias, float* y, uint8_t* argmax, cudaStream_t s);
+// the forward dispatcher (capi.cu), reused by the backward-input pass
+int dispatch_forward(const rc_desc& d, const float* x, const void* bank, const float* bias, float* y,
+                     uint8_t* am, void* ws, size_t ws_bytes, cudaStream_t s);
+// backward (backward.cu)
+size_t bwd_input_ws(const rc_desc& d);
+size_t bwd_weight_ws(const rc_desc& d);
+int launch_pool_backward(const rc_desc& d, const float* gy, const uint8_t* am, float* df, cudaStream_t s);
+int launch_bwd_input(const rc_desc& d, const float* df, const void* bank, float* dx, void* ws, cudaStream_t s);
+int launch_bwd_weight(const rc_desc& d, const float* x, const float* df, float* dw0, float* dw1, void* ws,
+                      cudaStream_t s);
+int launch_relu_backward(const float* y, float* gy, long long n, cudaStream_t s);
+int launch_bias_backward(const float* gy, float* db, int n, int cout, long long per, cudaStream_t s);
 // stack glue (stack.cu)
 int launch_maxpool2x2(int n, int c, int h, int w, const float* x, float* y, cudaStream_t s);
 int launch_gap_linear(int n, int c, int h, int w, const float* x, const float* wc, const float* bc, int classes,

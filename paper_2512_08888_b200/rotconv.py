@@ -514,3 +514,58 @@ def total_loss(ce, basis: SteerableBasis, lambda_mag: float, lambda_orth: float,
     if lambda_mag < 0 or lambda_orth < 0:
         raise ValueError("total_loss: lambdas must be >= 0")
     return ce + lambda_mag * loss_mag(basis) + lambda_orth * loss_orth(basis, eps)
+
+
+# ------------------------------------------------------------ backward
+def ri_conv_backward(desc: Desc, x: torch.Tensor, bank: torch.Tensor, gy: torch.Tensor,
+                     y: torch.Tensor | None = None, argmax: torch.Tensor | None = None,
+                     need_input: bool = True, need_weight: bool = True, need_bias: bool = True):
+    """Gradients of ri_conv_forward for the upstream gradient gy (N, Cout, R', H, W).
+
+    Returns (dx | None, dw0 | None, dw1 | None, dbias | None): dw0 = dW (single, p4, p4m) or
+    d f_x (steer), dw1 = d f_y (steer).  y (the forward output) is needed for ReLU layers,
+    argmax for max / subgroup pooling.  gy is not modified (a masked copy is used).
+    """
+    desc.validate()
+    x = _check_cuda_f32("x", x)
+    gy = _check_cuda_f32("gy", gy).clone()  # the C-ABI masks it in place for ReLU
+    dev = x.device
+    d = desc.c()
+    L = lib()
+    scratch = torch.empty(int(L.rc_backward_scratch_bytes(C.byref(d))) // 4 or 1, device=dev)
+    wsb = int(L.rc_backward_workspace_size(C.byref(d)))
+    ws = torch.empty(max(wsb, 1), dtype=torch.uint8, device=dev)
+    dx = torch.empty_like(x) if need_input else None
+    wshape = (desc.c_out, desc.c_in, desc.k, desc.k)
+    dw0 = torch.empty(wshape, device=dev) if need_weight else None
+    dw1 = torch.empty(wshape, device=dev) if (need_weight and desc.group == "steer") else None
+    db = torch.empty(desc.c_out, device=dev) if need_bias else None
+    check(L.rc_ri_conv_backward(C.byref(d), _ptr(x), _ptr(bank), _ptr(y), _ptr(gy), _ptr(argmax), _ptr(dx),
+                                _ptr(dw0), _ptr(dw1), _ptr(db), _ptr(scratch), _ptr(ws), C.c_size_t(wsb),
+                                _stream(dev)))
+    return dx, dw0, dw1, db
+
+
+class RIConvFunction(torch.autograd.Function):
+    """autograd bridge: y = fused RI layer(x; w0, w1, bias), backward through the C-ABI.
+
+    ``RIConvFunction.apply(x, w0, w1, bias, desc)``; returns the pooled output with the R'
+    axis kept, (N, Cout, R', H, W).  The argmax map is saved for the backward pass."""
+
+    @staticmethod
+    def forward(ctx, x, w0, w1, bias, desc: Desc):
+        bank = bank_precompute(desc, w0.detach(), None if w1 is None else w1.detach())
+        y, am = ri_conv_forward(desc, x.detach(), bank, None if bias is None else bias.detach())
+        ctx.desc = desc
+        ctx.has_w1 = w1 is not None
+        ctx.has_bias = bias is not None
+        ctx.save_for_backward(x.detach(), bank, y, am if am is not None else torch.empty(0, device=x.device))
+        return y
+
+    @staticmethod
+    def backward(ctx, gy):
+        x, bank, y, am = ctx.saved_tensors
+        dx, dw0, dw1, db = ri_conv_backward(
+            ctx.desc, x, bank, gy.contiguous(), y, am if am.numel() else None, ctx.needs_input_grad[0],
+            ctx.needs_input_grad[1] or ctx.needs_input_grad[2], ctx.has_bias and ctx.needs_input_grad[3])
+        return dx, dw0, (dw1 if ctx.has_w1 else None), db, None
