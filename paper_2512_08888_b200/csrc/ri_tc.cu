@@ -88,7 +88,8 @@ struct TcParams {
   float inv_r;  // 1/R for average pooling (R a power of two)
   int act;      // rc_activation applied after the bias (last op of the epilogue)
   int ablate;   // profiling only: 1 = skip stores, 2 = skip MMAs, 3 = skip MMAs + W loads,
-                // 4 = skip W loads (MMAs on stale tiles), 5 = epilogue skips TMEM loads + scatter
+                // 4 = skip W loads (MMAs on stale tiles), 5 = epilogue skips TMEM loads + scatter,
+                // 6 = 4 + 5 (the bare MMA issue stream)
 };
 
 // ---- TMEM -> registers ----------------------------------------------------------------
@@ -413,7 +414,7 @@ __device__ void epilogue(const TcParams& p, uint32_t tmem, uint64_t* d_full, uin
   for (int item = wk.first; item < wk.count; item += wk.stride) {
     const int n = wk.n(item), ct = wk.ct(item);
     const int co = ct * 128 + co_l;
-    if (p.ablate == 5) {  // profiling: consume D buffers without reading them
+    if (p.ablate == 5 || p.ablate == 6) {  // profiling: consume D buffers without reading them
       for (int i = 0; i < p.NB * p.NBK * 9; ++i) {
         mbar_wait(&d_full[e.db], e.dph);
         __syncwarp();
@@ -567,7 +568,7 @@ __global__ void __launch_bounds__(THREADS, 1) ri_tc_kernel(const __grid_constant
                 mbar_wait(&w_empty[wr.s], wr.ph ^ 1);
             }
             if (elect_one()) {
-              if (p.ablate == 3 || p.ablate == 4) {
+              if (p.ablate == 3 || p.ablate == 4 || p.ablate == 6) {
                 mbar_arrive(&w_full[wr.s]);  // profiling: no weight traffic
               } else {
                 mbar_arrive_expect_tx(&w_full[wr.s], stage_bytes);

@@ -43,9 +43,17 @@ __device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
       : "memory");
   return ok != 0;
 }
+#ifndef RC_MBAR_SUSPEND
+#define RC_MBAR_SUSPEND 1
+#endif
+__device__ __forceinline__ void mbar_wait_spin(uint64_t* bar, uint32_t parity);
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+#if RC_MBAR_SUSPEND
   while (!mbar_try_wait(bar, parity)) {
   }
+#else
+  mbar_wait_spin(bar, parity);
+#endif
 }
 // try_wait without the suspend-time hint: for barriers completed by REMOTE (other-CTA)
 // arrivals, where a suspended waiter is not woken promptly

@@ -42,7 +42,7 @@ __global__ void __launch_bounds__(128, 1)
     sA[sw128_offset(i / 64, i % 64) / 2] = Ag[i];
     sA[ATILE / 2 + sw128_offset(i / 64, i % 64) / 2] = Ag[i];
   }
-  const int nb = MODE >= 2 ? 8 : 1;
+  const int nb = MODE >= 2 ? 8 : 1;  // B tiles
   for (int t = 0; t < nb; ++t)
     for (int i = tid; i < N * 64; i += blockDim.x)
       reinterpret_cast<__nv_bfloat16*>(sB + t * BTILE)[sw128_offset(i / 64, i % 64) / 2] = Bg[i];
@@ -74,9 +74,49 @@ __global__ void __launch_bounds__(128, 1)
   tc_fence_after();
   const uint32_t idesc = idesc_bf16_f32(128, N);
   const uint64_t da = desc_k_sw128(smem_u32(sA)), db = desc_k_sw128(smem_u32(sB));
+  __shared__ uint64_t full7[8], empty7[8];
+  if (MODE >= 700 && tid == 0) {
+    for (int i = 0; i < 8; ++i) {
+      mbar_init(&full7[i], 1);
+      mbar_init(&empty7[i], 1);
+    }
+    fence_barrier_init();
+  }
+  __syncthreads();
   long long t0 = clock64();
+  if (MODE >= 700 && tid == 32) {
+    // producer warp: stage s may be (re)filled once the MMAs of its previous use completed
+    constexpr int DEPTH = (MODE / 10) % 10, SC = MODE % 10;
+    const int stages = (iters / 3) / SC;
+    for (int st = 0; st < stages; ++st) {
+      const int sidx = st % DEPTH;
+      if (st >= DEPTH) mbar_wait(&empty7[sidx], ((st / DEPTH) - 1) & 1);
+      mbar_arrive(&full7[sidx]);
+    }
+  }
   if (tid == 0) {
-    if (MODE == 0) {
+    if (MODE >= 700) {
+      constexpr int DEPTH = (MODE / 10) % 10, SC = MODE % 10;
+      const uint64_t dal = desc_k_sw128(smem_u32(sA) + ATILE);
+      const int stages = (iters / 3) / SC;
+      int it = 0;
+      for (int st = 0; st < stages; ++st) {
+        const int sidx = st % DEPTH;
+        mbar_wait(&full7[sidx], (st / DEPTH) & 1);
+        for (int q = 0; q < SC; ++q, ++it) {
+          const int c = it % 4, tap = (it / 4) % 4;
+          const uint32_t dd = d + tap * N;
+          const uint64_t bh = db + ((c * BTILE) >> 4), bl = db + (((c + 4) * BTILE) >> 4);
+#pragma unroll
+          for (int kk = 0; kk < 4; ++kk) mma_bf16_ss(dd, da + 2 * kk, bh + 2 * kk, idesc, (c | kk) != 0);
+#pragma unroll
+          for (int kk = 0; kk < 4; ++kk) mma_bf16_ss(dd, da + 2 * kk, bl + 2 * kk, idesc, 1);
+#pragma unroll
+          for (int kk = 0; kk < 4; ++kk) mma_bf16_ss(dd, dal + 2 * kk, bh + 2 * kk, idesc, 1);
+        }
+        mma_commit(&empty7[sidx]);
+      }
+    } else if (MODE == 0) {
       for (int it = 0; it < iters; ++it)
 #pragma unroll
         for (int kk = 0; kk < 4; ++kk) mma_bf16_ss(d, da + 2 * kk, db + 2 * kk, idesc, (it | kk) != 0);
@@ -84,6 +124,92 @@ __global__ void __launch_bounds__(128, 1)
       for (int it = 0; it < iters; ++it)
 #pragma unroll
         for (int kk = 0; kk < 4; ++kk) mma_bf16_ts(d, a_tm + kk * 8, db + 2 * kk, idesc, (it | kk) != 0);
+    } else if (MODE >= 100) {
+      // ring of DEPTH commit barriers, one commit per stage of SC chunks (12 MMAs each);
+      // before committing stage i, wait for the commit of stage i - DEPTH (the kernel's
+      // W-ring dependency without any loads)
+      constexpr int DEPTH = (MODE / 10) % 10, SC = MODE % 10;  // MODE = 100/200/300 + ...
+      const uint64_t dal = desc_k_sw128(smem_u32(sA) + ATILE);
+      __shared__ uint64_t rb[8];
+      for (int i = 0; i < DEPTH; ++i) mbar_init(&rb[i], 1);
+      mbar_init(&rb[7], 1);
+      fence_barrier_init();
+      mbar_arrive(&rb[7]);  // phase 0 complete
+      uint32_t phase[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+      int stage = 0;
+      for (int it = 0; it < iters / 3; ++it) {
+        const int c = it % 4, tap = (it / 4) % 4;
+        const uint32_t dd = d + tap * N;
+        const uint64_t bh = db + ((c * BTILE) >> 4), bl = db + (((c + 4) * BTILE) >> 4);
+        if (MODE >= 400 && it % SC == 0) {
+          // wait on a barrier nobody's MMAs complete: initialised with count 1 and arrived
+          // once by this thread, so every try_wait on phase 0 succeeds immediately
+          if constexpr (MODE >= 500) {
+            uint32_t ok = 0;
+            while (!ok) {
+              asm volatile("{\n.reg .pred p;\nmbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\nselp.u32 %0, 1, 0, p;\n}\n"
+                           : "=r"(ok) : "r"(smem_u32(&rb[7])), "r"(0u) : "memory");
+            }
+          } else {
+            while (!mbar_try_wait(&rb[7], 0)) {}
+          }
+        } else if (it % SC == 0 && stage >= DEPTH) {
+          const int sidx = stage % DEPTH;
+          if constexpr (MODE >= 300) {  // test_wait (non-blocking probe) in a spin loop
+            uint32_t ok = 0;
+            while (!ok) {
+              asm volatile("{\n.reg .pred p;\nmbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\nselp.u32 %0, 1, 0, p;\n}\n"
+                           : "=r"(ok) : "r"(smem_u32(&rb[sidx])), "r"(phase[sidx]) : "memory");
+            }
+          } else if constexpr (MODE >= 200) {  // try_wait without the suspend hint
+            mbar_wait_spin(&rb[sidx], phase[sidx]);
+          } else {
+            while (!mbar_try_wait(&rb[sidx], phase[sidx])) {}
+          }
+          phase[sidx] ^= 1;
+        }
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk) mma_bf16_ss(dd, da + 2 * kk, bh + 2 * kk, idesc, (c | kk) != 0);
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk) mma_bf16_ss(dd, da + 2 * kk, bl + 2 * kk, idesc, 1);
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk) mma_bf16_ss(dd, dal + 2 * kk, bh + 2 * kk, idesc, 1);
+        if (it % SC == SC - 1) {
+          if (MODE < 400) mma_commit(&rb[stage % DEPTH]);
+          ++stage;
+        }
+      }
+    } else if (MODE == 5 || MODE == 6) {
+      // the RI kernel's stream: 3 MMAs x 4 kk per chunk, commit every 2 chunks (a W stage),
+      // D buffer switch every 4 chunks (a tap); MODE 6 adds an mbarrier wait per stage
+      const uint64_t dal = desc_k_sw128(smem_u32(sA) + ATILE);
+      __shared__ uint64_t cb[4];
+      if (true) {
+        for (int i = 0; i < 4; ++i) mbar_init(&cb[i], 1);
+        fence_barrier_init();
+      }
+      uint32_t phase[4] = {0, 0, 0, 0};
+      int used[4] = {0, 0, 0, 0};
+      for (int it = 0; it < iters / 3; ++it) {
+        const int c = it % 4, tap = (it / 4) % 4;
+        const uint32_t dd = d + tap * N;
+        const uint64_t bh = db + ((c * BTILE) >> 4), bl = db + (((c + 4) * BTILE) >> 4);
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk) mma_bf16_ss(dd, da + 2 * kk, bh + 2 * kk, idesc, (c | kk) != 0);
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk) mma_bf16_ss(dd, da + 2 * kk, bl + 2 * kk, idesc, 1);
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk) mma_bf16_ss(dd, dal + 2 * kk, bh + 2 * kk, idesc, 1);
+        if (c % 2 == 1) {
+          const int sidx = (it / 2) % 2;
+          if (MODE == 6 && used[sidx]) {  // wait the stage's previous commit (ring of 2)
+            while (!mbar_try_wait(&cb[sidx], phase[sidx])) {}
+            phase[sidx] ^= 1;
+          }
+          mma_commit(&cb[sidx]);
+          used[sidx] = 1;
+        }
+      }
     } else if (MODE == 3 || MODE == 4) {
       // W_hi (MODE 3) or W_hi and W_lo (MODE 4) staged smem -> TMEM with tcgen05.cp per
       // K-step, consumed by TS MMAs in issue order; double-buffered TMEM A regions
@@ -192,9 +318,9 @@ void run() {
   CK(cudaMemcpy(&cyc, dcyc, 8, cudaMemcpyDeviceToHost));
   const int mmas = MODE >= 2 ? (iters / 3) * 12 : iters * 4;
   const double per = (double)cyc / mmas;
-  printf("{\"test\":\"%s\",\"M\":128,\"N\":%d,\"correct\":%s,\"mismatches\":%d,\"cycles_per_mma_k16\":%.2f,"
+  printf("{\"mode\":%d,\"test\":\"%s\",\"M\":128,\"N\":%d,\"correct\":%s,\"mismatches\":%d,\"cycles_per_mma_k16\":%.2f,"
          "\"macs_per_cycle\":%.1f,\"math_cycles\":%.1f}\n",
-         MODE == 0 ? "mma_ss" : MODE == 1 ? "mma_ts" : MODE == 2 ? "pattern_bf16x3_ss" : MODE == 3 ? "pattern_bf16x3_whi_tmem" : "pattern_bf16x3_w_tmem", N, bad == 0 ? "true" : "false", bad, per,
+         MODE, MODE == 0 ? "mma_ss" : MODE == 1 ? "mma_ts" : MODE == 2 ? "pattern_bf16x3_ss" : MODE == 3 ? "pattern_bf16x3_whi_tmem" : MODE == 4 ? "pattern_bf16x3_w_tmem" : MODE == 5 ? "kernel_stream_commits" : MODE == 6 ? "kernel_stream_commits_waits" : "commit_ring_depth_x10_plus_chunks_per_stage", N, bad == 0 ? "true" : "false", bad, per,
          128.0 * N * 16 / per, 128.0 * N * 16 / 4096);
   cudaFree(dA);
   cudaFree(dB);
@@ -203,17 +329,10 @@ void run() {
 }
 
 int main() {
-  run<64, 0>();
   run<96, 0>();
-  run<96, 1>();
-  run<96, 2>();
-  run<96, 3>();
-  run<96, 4>();
-  run<112, 3>();
-  run<112, 4>();
-  run<128, 3>();
-  run<128, 4>();
-  run<64, 3>();
-  run<64, 4>();
+  run<96, 722>();
+  run<96, 742>();
+  run<96, 744>();
+  run<96, 784>();
   return 0;
 }
