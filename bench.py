@@ -165,6 +165,40 @@ def run_reference(args, wl):
     print(json.dumps(out), flush=True)
 
 
+def cudnn_context(P, desc, x, fx, fy, ours_ms, args):
+    """Context only (not the product path): the same R orientation slices
+    as R separate cuDNN convolutions on the rotated kernels (the paper's cuDNN RI pipeline),
+    unpooled, FP32 and TF32-allowed, on this B200.  Our step above also pools + biases."""
+    import torch
+    import torch.nn.functional as F
+    k, R = desc.k, desc.orientations
+    kern = P.rotconv.build_orientation_bank_from(desc, fx, fy if desc.group == "steer" else None)
+    wcat = torch.flip(kern, dims=(3, 4)).reshape(R * desc.c_out, desc.c_in, k, k).contiguous()
+    torch.backends.cudnn.benchmark = True
+    out = {}
+    for name, tf32 in (("fp32", False), ("tf32", True)):
+        torch.backends.cudnn.allow_tf32 = tf32
+        for _ in range(3):
+            F.conv2d(x, wcat, padding=k // 2)
+        torch.cuda.synchronize()
+        ts = []
+        for _ in range(5):
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            F.conv2d(x, wcat, padding=k // 2)
+            b.record()
+            b.synchronize()
+            ts.append(a.elapsed_time(b))
+        out[f"cudnn_{name}_ms"] = statistics.median(ts)
+    torch.backends.cudnn.allow_tf32 = False
+    out["ours_ms"] = ours_ms
+    out["speedup_vs_cudnn_fp32"] = out["cudnn_fp32_ms"] / ours_ms
+    out["speedup_vs_cudnn_tf32"] = out["cudnn_tf32_ms"] / ours_ms
+    out["note"] = ("R separate cuDNN convs (unpooled, batch in HBM) vs this repo's fused layer "
+                   "(reuse scatter + subgroup pooling + argmax + bias); context, not the product path")
+    return out
+
+
 def _stack_cpu_sample(threads, n_img=2):
     """Oracle composition of the C5 stack on a bounded sample (tests/test_gpu_stack.py)."""
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
@@ -333,6 +367,7 @@ def main():
     ap.add_argument("--precision", default="auto", choices=["fp32", "bf16x3", "bf16", "auto"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--no-cudnn", action="store_true", help="skip the cuDNN context measurement")
     args = ap.parse_args()
     wl = WORKLOADS[args.workload]
     if args.impl == "reference":
@@ -439,6 +474,9 @@ def main():
     if os.path.exists(prof):
         tr = json.load(open(prof)).get(f"{args.workload}:{desc.kernel_name()}")
         traffic = tr
+    cudnn_ctx = None
+    if rank == 0 and world == 1 and not args.no_cudnn:
+        cudnn_ctx = cudnn_context(P, desc, x, fx, fy, ms, args)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         v, info = cpu_reference(wl, os.cpu_count() or 1)
@@ -475,6 +513,7 @@ def main():
             "gpu_launches": args.steps * (2 if desc.kernel_name().startswith("tc_") else 1),
             "gpu_launches_note": "per step: tc path = x_pack_kernel + ri_tc_kernel; SIMT = one fused kernel",
             "cpu_baseline": cpu,
+            "cudnn_context": cudnn_ctx,
             "timed_output_matches_e2e": bool(ok),
         }
         print(json.dumps(out), flush=True)
