@@ -246,29 +246,33 @@ __device__ __forceinline__ void tmem_ld2f(uint32_t taddr, float& a, float& b) {
   b = __uint_as_float(r1);
 }
 
+// one input row of the thread's window: 16 columns + (TW = 32, strips) the halo columns.
+// issue_row only issues the TMEM loads; finish_row (after tcgen05.wait::ld) fixes edges.
 template <int TW>
-__device__ __forceinline__ void load_row(uint32_t a, int half, float (&z)[18]) {
-  float v[16];
+__device__ __forceinline__ void issue_row(uint32_t a, float (&z)[18]) {
   if constexpr (TW == 0) {  // strip: the band row holds the halo columns (zero at image edges)
-    tmem_ld16(a, v);
+    tmem_ld16(a, *reinterpret_cast<float(*)[16]>(&z[0]));
     tmem_ld2f(a + 16, z[16], z[17]);
-    tmem_wait_ld();
-#pragma unroll
-    for (int i = 0; i < 16; ++i) z[i] = v[i];
-    return;
+  } else {
+    tmem_ld16(a, *reinterpret_cast<float(*)[16]>(&z[1]));
+    if (TW == 32) {
+      z[0] = tmem_ld1(a - 1);
+      z[17] = tmem_ld1(a + 16);
+    }
   }
-  tmem_ld16(a, v);
-  if (TW == 32) {
-    z[0] = tmem_ld1(a - 1);
-    z[17] = tmem_ld1(a + 16);
-  }
-  tmem_wait_ld();
-#pragma unroll
-  for (int i = 0; i < 16; ++i) z[1 + i] = v[i];
+}
+template <int TW>
+__device__ __forceinline__ void finish_row(int half, float (&z)[18]) {
   if (TW == 32) {  // image edges: the neighbouring half does not exist
     if (half == 0) z[0] = 0.f;
     if (half == TW / 16 - 1) z[17] = 0.f;
   }
+}
+template <int TW>
+__device__ __forceinline__ void load_row(uint32_t a, int half, float (&z)[18]) {
+  issue_row<TW>(a, z);
+  tmem_wait_ld();
+  finish_row<TW>(half, z);
 }
 
 // small images: window row I (input row o0 - 1 + I) feeds output row i of the thread's TR
@@ -357,10 +361,16 @@ __device__ __forceinline__ void epi_tap(EpiState& e, float (&Y)[RPB][XH], uint64
     }
     return;
   }
-  load_row<TW>(a, e.half, z);
-  scatter_row<TW, RPB, CONV, T, 0>(Y, z);
-  load_row<TW>(a + Geo<TW>::RS, e.half, z);
-  scatter_row<TW, RPB, CONV, T, 1>(Y, z);
+  {  // rows 0 and 1 in flight together: one TMEM round trip instead of two
+    float z1[18];
+    issue_row<TW>(a, z);
+    issue_row<TW>(a + Geo<TW>::RS, z1);
+    tmem_wait_ld();
+    finish_row<TW>(e.half, z);
+    finish_row<TW>(e.half, z1);
+    scatter_row<TW, RPB, CONV, T, 0>(Y, z);
+    scatter_row<TW, RPB, CONV, T, 1>(Y, z1);
+  }
   load_row<TW>(a + 2 * Geo<TW>::RS, e.half, z);
   tc_fence_before();
   __syncwarp();
