@@ -31,12 +31,16 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
+STRONG = {"c4", "c5"}  # fixed global batch split over the ranks; c1/c3: fixed batch per rank
 WORKLOADS = {
     # name: (n per rank, cin, h, w, cout, k, group, R, pool, pool_group, label)
     "c3": (256, 256, 16, 16, 1024, 3, "steer", 8, "subgroup", 4,
            "C3: RI conv 16x16x256->1024, steerable R=8 (2 bases), subgroup-4 max+argmax+bias"),
+    # C4: global batch 512 sharded over the ranks (BASELINE.json: "batch 512, batch-sharded
+    # over 2/4/8 GPUs") -> strong scaling
     "c4": (512, 128, 32, 32, 512, 3, "steer", 16, "subgroup", 4,
-           "C4: RI conv 32x32x128->512, steerable R=16 (4 bases), subgroup-4 max+argmax+bias"),
+           "C4: RI conv 32x32x128->512, steerable R=16 (4 bases), subgroup-4 max+argmax+bias, "
+           "global batch 512 sharded over the GPUs"),
     "c1": (32, 64, 8, 8, 256, 3, "single", 1, "none", 1,
            "C1: single-orientation scatter conv 8x8x64->256"),
     # C5: the multi-layer RI classifier (paper_2512_08888_b200/stack.py), global batch 1024
@@ -389,6 +393,11 @@ def main():
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
     n, cin, h, w, cout, k, g, R, pool, pg, label = wl
+    strong = args.workload in STRONG
+    n_global = n if strong else n * world
+    if strong:  # this rank's contiguous shard of the global batch (rc_shard_range)
+        b0, b1 = P.shard_range(n, world, rank)
+        n = b1 - b0
     desc = P.Desc(n, cin, h, w, cout, k, g, R, pool, pg, "scatter", args.precision)
     gen = torch.Generator(device=dev).manual_seed(1234)  # same weights on every rank
     s = 1 / np.sqrt(cin * k * k)
@@ -436,7 +445,7 @@ def main():
     if world > 1:
         dist.all_reduce(tot, op=dist.ReduceOp.MAX)
     ms = tot.item() / args.steps
-    eff_total = desc.eff_flops() * world
+    eff_total = 2 * n_global * h * w * k * k * cin * cout * R  # all ranks' images
     value = eff_total / (ms * 1e-3) / 1e12
     alg = desc.alg_flops()
     achieved = alg / ((kernel_ms or statistics.mean(times)) * 1e-3) / 1e12
@@ -486,9 +495,10 @@ def main():
         out = {
             "metric": "RI-conv layer effective TFLOP/s", "value": value, "unit": "TFLOP/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+            "higher_is_better": True, "scaling": "strong" if strong else "weak", "vs_baseline": None,
+            "dtype": "f32",
             "data": "synthetic (uniform[-1,1) inputs, uniform/sqrt(Cin*K^2) weights, random init)",
-            "config": {"workload": label, "n_per_gpu": n, "c_in": cin, "h": h, "w": w,
+            "config": {"workload": label, "n_per_gpu": n, "global_batch": n_global, "c_in": cin, "h": h, "w": w,
                        "c_out": cout, "k": k, "group": g, "orientations": R, "pool": pool,
                        "pool_group": pg, "precision": args.precision, "kernel": desc.kernel_name(),
                        "l2": "flushed between timed iterations (512 MB write)",
