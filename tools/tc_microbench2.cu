@@ -42,7 +42,7 @@ __global__ void __launch_bounds__(128, 1)
     sA[sw128_offset(i / 64, i % 64) / 2] = Ag[i];
     sA[ATILE / 2 + sw128_offset(i / 64, i % 64) / 2] = Ag[i];
   }
-  const int nb = MODE >= 2 ? 8 : 1;  // B tiles
+  const int nb = MODE == 8 ? 8 : (MODE >= 2 ? 8 : 1);  // B tiles
   for (int t = 0; t < nb; ++t)
     for (int i = tid; i < N * 64; i += blockDim.x)
       reinterpret_cast<__nv_bfloat16*>(sB + t * BTILE)[sw128_offset(i / 64, i % 64) / 2] = Bg[i];
@@ -124,6 +124,17 @@ __global__ void __launch_bounds__(128, 1)
       for (int it = 0; it < iters; ++it)
 #pragma unroll
         for (int kk = 0; kk < 4; ++kk) mma_bf16_ts(d, a_tm + kk * 8, db + 2 * kk, idesc, (it | kk) != 0);
+    } else if (MODE == 8) {
+      const uint32_t idesc2 = idesc_bf16_f32(128, 2 * N);
+      const uint64_t dal = desc_k_sw128(smem_u32(sA) + ATILE);
+      for (int it = 0; it < iters / 3; ++it) {
+        const int c = it % 4;
+        const uint64_t bhl = db + ((c * 2 * BTILE) >> 4);  // [hi | lo] contiguous, 2N rows
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk) mma_bf16_ss(d, da + 2 * kk, bhl + 2 * kk, idesc2, (it | kk) != 0);
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk) mma_bf16_ss(d, dal + 2 * kk, bhl + 2 * kk, idesc, 1);
+      }
     } else if (MODE >= 100) {
       // ring of DEPTH commit barriers, one commit per stage of SC chunks (12 MMAs each);
       // before committing stage i, wait for the commit of stage i - DEPTH (the kernel's
@@ -329,10 +340,11 @@ void run() {
 }
 
 int main() {
-  run<96, 0>();
-  run<96, 722>();
-  run<96, 742>();
-  run<96, 744>();
-  run<96, 784>();
+  run<96, 2>();
+  run<96, 8>();
+  run<112, 2>();
+  run<112, 8>();
+  run<64, 2>();
+  run<64, 8>();
   return 0;
 }
