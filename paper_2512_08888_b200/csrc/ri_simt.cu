@@ -20,6 +20,7 @@
 // Each channel dot accumulates in ascending ci with FFMA; each output adds its 9 taps in
 // a fixed order, so dyadic inputs reproduce the oracle bit-for-bit (tests/test_gpu_parity).
 #include <algorithm>
+#include <cstdlib>
 
 #include "k3_tables.cuh"
 #include "rc_internal.cuh"
@@ -347,12 +348,16 @@ int launch_simt_k3(const rc_desc& d, const float* x, const void* bank, const flo
                    float* y, uint8_t* argmax, cudaStream_t s, bool dry_run, const char** name) {
   if (d.k != 3) return RC_ERR_UNSUPPORTED;
   int SW, S;
+  // SW columns per thread: 8 keeps more work per thread, 4 halves the register state
+  // (3-row x 4-rotation accumulators) so more warps fit per SM; RC_SIMT_SW selects (A/B)
+  const char* swe = getenv("RC_SIMT_SW");
+  const int sw_pref = swe ? atoi(swe) : 8;
   switch (d.w) {
     case 4: SW = 4; S = 1; break;
-    case 8: SW = 8; S = 1; break;
-    case 16: SW = 8; S = 2; break;
-    case 32: SW = 8; S = 4; break;
-    case 64: SW = 8; S = 8; break;
+    case 8: SW = sw_pref == 4 ? 4 : 8; S = 8 / SW; break;
+    case 16: SW = sw_pref == 4 ? 4 : 8; S = 16 / SW; break;
+    case 32: SW = sw_pref == 4 ? 4 : 8; S = 32 / SW; break;
+    case 64: SW = sw_pref == 4 ? 4 : 8; S = 64 / SW; break;
     default: return RC_ERR_UNSUPPORTED;
   }
   // CTA shape: threads = COB * S * IMG <= 256; prefer >= 2 waves of CTAs over 148 SMs.
@@ -393,8 +398,16 @@ int launch_simt_k3(const rc_desc& d, const float* x, const void* bank, const flo
   const size_t smem = 2 * sizeof(float) * ((size_t)IMG * CC * d.w + (size_t)CC * COB * 12);
   const int gx = (d.c_out + COB - 1) / COB, gy = (d.n + IMG - 1) / IMG;
   if (gy > 65535) return RC_ERR_UNSUPPORTED;
+  if (SW == 4) {
+    switch (d.w) {
+      case 4: return launch_rc<4, 1>(d, p, gx, gy, threads, smem, s);
+      case 8: return launch_rc<4, 2>(d, p, gx, gy, threads, smem, s);
+      case 16: return launch_rc<4, 4>(d, p, gx, gy, threads, smem, s);
+      case 32: return launch_rc<4, 8>(d, p, gx, gy, threads, smem, s);
+      default: return launch_rc<4, 16>(d, p, gx, gy, threads, smem, s);
+    }
+  }
   switch (d.w) {
-    case 4: return launch_rc<4, 1>(d, p, gx, gy, threads, smem, s);
     case 8: return launch_rc<8, 1>(d, p, gx, gy, threads, smem, s);
     case 16: return launch_rc<8, 2>(d, p, gx, gy, threads, smem, s);
     case 32: return launch_rc<8, 4>(d, p, gx, gy, threads, smem, s);
