@@ -2,7 +2,7 @@
 # round-1 evidence pass: tests, smoke, C++ API, bench lines C1/C3/C4/C5 (+fp32/bf16 rows),
 # reference arm, C2 sweep, ncu launch lists and full captures of the dominant kernels
 cd "${GRAFT_REPO_ROOT:-.}"
-O=gpurun_out/final
+O=gpurun_out/final2
 mkdir -p $O/c2
 nvidia-smi > $O/nvidia_smi.txt 2>&1
 timeout -s KILL 1500 python -m pytest tests -m gpu -q --timeout 600 > $O/pytest_gpu.log 2>&1; echo "rc=$?" >> $O/pytest_gpu.log
