@@ -51,6 +51,15 @@ WORKLOADS = {
 }
 
 
+def arith_dtype(kernel: str) -> str:
+    """Arithmetic the timed kernel computes in (not a precision claim)."""
+    if kernel.startswith("tc_") and kernel.endswith("bf16x3"):
+        return "bf16x3 (3 bf16 MMA products, f32 accumulate)"
+    if kernel.startswith("tc_"):
+        return "bf16 (f32 accumulate)"
+    return "f32"
+
+
 def peaks():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(p):
@@ -333,7 +342,8 @@ def run_stack(args, wl):
         out = {
             "metric": "RI classifier forward effective TFLOP/s", "value": value, "unit": "TFLOP/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
-            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": "mixed: " + ", ".join(sorted({arith_dtype(k) for k in stack.kernels(n)})),
             "data": "synthetic (uniform[-1,1) images, random-init weights)",
             "config": {"workload": wl[-1], "global_batch": n_total, "batch_per_gpu": n,
                        "precision": args.precision, "kernels": stack.kernels(n),
@@ -496,7 +506,7 @@ def main():
             "metric": "RI-conv layer effective TFLOP/s", "value": value, "unit": "TFLOP/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
             "higher_is_better": True, "scaling": "strong" if strong else "weak", "vs_baseline": None,
-            "dtype": "f32",
+            "dtype": arith_dtype(desc.kernel_name()),
             "data": "synthetic (uniform[-1,1) inputs, uniform/sqrt(Cin*K^2) weights, random init)",
             "config": {"workload": label, "n_per_gpu": n, "global_batch": n_global, "c_in": cin, "h": h, "w": w,
                        "c_out": cout, "k": k, "group": g, "orientations": R, "pool": pool,

@@ -1,4 +1,4 @@
-"""World-size-2 gloo test of the batch-sharded driver's host logic (shard ranges +
+"""World-size-2/4 gloo test of the batch-sharded driver's host logic (shard ranges +
 ragged output gather).  The per-shard compute is the CPU oracle (test infrastructure);
 on the GPU box the same gather runs over NCCL (bench.py --gpus N)."""
 import os
@@ -50,12 +50,12 @@ def _worker(rank, world, port, n, q):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("n", [6, 5])  # even and ragged shards
-def test_two_rank_shard_and_gather(n):
+@pytest.mark.parametrize("world,n", [(2, 6), (2, 5), (4, 6)])  # even, ragged, and a 4-rank split
+def test_rank_shard_and_gather(world, n):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    ps = [ctx.Process(target=_worker, args=(r, 2, port, n, q)) for r in range(2)]
+    ps = [ctx.Process(target=_worker, args=(r, world, port, n, q)) for r in range(world)]
     for p in ps:
         p.start()
     res = [q.get(timeout=120) for _ in ps]
@@ -64,4 +64,6 @@ def test_two_rank_shard_and_gather(n):
         assert p.exitcode == 0
     assert all(r[0] and r[1] for r in res), res
     spans = sorted(r[2] for r in res)
-    assert spans[0][0] == 0 and spans[-1][1] == n and spans[0][1] == spans[1][0]
+    assert spans[0][0] == 0 and spans[-1][1] == n
+    assert all(spans[i][1] == spans[i + 1][0] for i in range(len(spans) - 1))  # contiguous cover
+    assert max(e - b for b, e in spans) - min(e - b for b, e in spans) <= 1   # balanced

@@ -16,6 +16,7 @@ timeout -s KILL 900 python bench.py --workload c5 --steps 10 --warmup 3 > $O/ben
 timeout -s KILL 300 python bench.py --workload c1 > $O/bench_c1.json 2> $O/bench_c1.err
 timeout -s KILL 900 python bench.py --impl reference --steps 3 --warmup 1 > $O/bench_ref_c3.json 2> $O/bench_ref_c3.err
 timeout -s KILL 1500 python tools/appendix_sweep.py --out $O/c2 > $O/c2/sweep.log 2>&1; echo rc=$? >> $O/c2/sweep.log
+timeout -s KILL 1500 python tools/bench_cli.py --sizes 8 16 32 --cin 64 256 --cout 256 1024 --orientations 8 --group steer --batch 32 --out $O/bench_cli_r8.md --format md > $O/bench_cli_r8.log 2>&1; echo rc=$? >> $O/bench_cli_r8.log
 NCU=/usr/local/cuda/bin/ncu
 for w in c3 c4 c1; do
 timeout -s KILL 600 $NCU --metrics gpu__time_duration.sum --clock-control none -c 60 --csv --log-file $O/launches_$w.csv \
