@@ -170,8 +170,10 @@ def run_reference(args, wl):
     out = {"impl": "reference", "metric": "RI-conv layer effective TFLOP/s", "value": v,
            "unit": "TFLOP/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
            "ms_per_step": info["ms_full_layer_extrapolated"], "higher_is_better": True,
-           "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-           "config": {"workload": label, "n": n, "orientations": R, "host_threads": threads},
+           "scaling": "strong" if args.workload in STRONG else "weak", "vs_baseline": None,
+           "dtype": "f32", "data": "synthetic",
+           "config": {"workload": label, "n": n, "orientations": R, "host_threads": threads,
+                      "note": "one host runs the whole workload (the reference has no GPUs)"},
            "cpu_baseline": {"value": v, "unit": "TFLOP/s", "cores": threads, "kind": info["kind"],
                             "sample": info["sample"]},
            "e2e": {"value": v, "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
