@@ -59,7 +59,7 @@ struct Geo {
   static constexpr int MMA_N = (BAND_PX + 15) / 16 * 16;
   static constexpr int XTILE = MMA_N * 64 * 2;                // bytes of one [MMA_N x 64 ci] bf16 tile
   static constexpr int HALVES = (STRIP || SMALL) ? 1 : TW / 16;  // epilogue threads per output row
-  static constexpr int NDB = MMA_N * 4 + 16 <= 512 ? 4 : 3;   // TMEM D buffers
+  static constexpr int NDB = MMA_N * 5 + 16 <= 512 ? 5 : (MMA_N * 4 + 16 <= 512 ? 4 : 3);  // TMEM D buffers
   static constexpr int TR = SMALL ? 16 / TW : 1;              // output rows per epilogue thread
   static constexpr int IMGS = SMALL ? 64 / (TW * TW) : 1;     // images per band
 };
@@ -70,7 +70,7 @@ constexpr int EPI_WARP0 = 4;             // warps 0-3: producer warpgroup (TMA, 
 constexpr int THREADS = 32 * (EPI_WARP0 + NUM_EPI);
 constexpr int REGS_PRODUCER = 32;        // setmaxnreg budgets: 20 warps x 96 at launch
 constexpr int REGS_EPILOGUE = 112;
-constexpr int MAX_NDB = 4;
+constexpr int MAX_NDB = 5;
 constexpr int MAX_NC = 8;                // ci chunks of 64 (Cin <= 512)
 constexpr uint32_t D0 = 16;              // D buffers from column 16: the 1-column-left halo
                                          // load of a band's first pixel stays in the allocation
