@@ -59,7 +59,11 @@ struct Geo {
   static constexpr int MMA_N = (BAND_PX + 15) / 16 * 16;
   static constexpr int XTILE = MMA_N * 64 * 2;                // bytes of one [MMA_N x 64 ci] bf16 tile
   static constexpr int HALVES = (STRIP || SMALL) ? 1 : TW / 16;  // epilogue threads per output row
-  static constexpr int NDB = MMA_N * 5 + 16 <= 512 ? 5 : (MMA_N * 4 + 16 <= 512 ? 4 : 3);  // TMEM D buffers
+  // D buffers from column D0.  Columns [0, D0) keep the 1-column-left halo load of a band's
+  // first pixel inside the allocation; full-row bands also read their skipped (out-of-image)
+  // window rows from them as zeros (band_rows), so they need D0 >= 18.
+  static constexpr uint32_t D0 = (STRIP || SMALL) ? 16 : 32;
+  static constexpr int NDB = MMA_N * 5 + D0 <= 512 ? 5 : (MMA_N * 4 + D0 <= 512 ? 4 : 3);  // TMEM D buffers
   static constexpr int TR = SMALL ? 16 / TW : 1;              // output rows per epilogue thread
   static constexpr int IMGS = SMALL ? 64 / (TW * TW) : 1;     // images per band
 };
@@ -72,9 +76,15 @@ constexpr int REGS_PRODUCER = 32;        // setmaxnreg budgets: 20 warps x 96 at
 constexpr int REGS_EPILOGUE = 112;
 constexpr int MAX_NDB = 5;
 constexpr int MAX_NC = 8;                // ci chunks of 64 (Cin <= 512)
-constexpr uint32_t D0 = 16;              // D buffers from column 16: the 1-column-left halo
-                                         // load of a band's first pixel stays in the allocation
 constexpr int XH = 16;                   // output columns per epilogue thread
+
+// Input rows [first, end) of full-row band k (band rows 0 .. IN_ROWS-1 = image rows
+// OUT_ROWS*k - 1 ...) that lie inside the image; the others are the zero padding.
+template <int TW>
+__device__ __forceinline__ int2 band_rows(int k, int H) {
+  const int r0 = Geo<TW>::OUT_ROWS * k - 1;
+  return make_int2(r0 < 0 ? -r0 : 0, min(Geo<TW>::IN_ROWS, H - r0));
+}
 
 struct TcParams {
   const uint8_t* xh;  // packed X tiles [n][band][chunk] (hi), 12 KB each
@@ -90,6 +100,7 @@ struct TcParams {
   int ablate;   // profiling only: 1 = skip stores, 2 = skip MMAs, 3 = skip MMAs + W loads,
                 // 4 = skip W loads (MMAs on stale tiles), 5 = epilogue skips TMEM loads + scatter,
                 // 6 = 4 + 5 (the bare MMA issue stream)
+  int trim;     // full-row bands skip their out-of-image halo rows (band_rows); 0 = A/B switch
 };
 
 // ---- TMEM -> registers ----------------------------------------------------------------
@@ -232,6 +243,13 @@ __device__ __forceinline__ void scatter_row(float (&Y)[RPB][XH], const float (&z
   }
 }
 
+__device__ __forceinline__ void tmem_zero32(uint32_t taddr) {  // columns [0, 32) of the warp's lanes
+#pragma unroll
+  for (int c = 0; c < 32; c += 8)
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%1,%1,%1,%1,%1,%1,%1};\n" ::"r"(taddr + c), "r"(0u)
+                 : "memory");
+  asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
+}
 __device__ __forceinline__ float tmem_ld1(uint32_t taddr) {
   uint32_t r;
   asm volatile("tcgen05.ld.sync.aligned.32x32b.x1.b32 {%0}, [%1];\n" : "=r"(r) : "r"(taddr));
@@ -326,6 +344,8 @@ struct EpiState {
   int lane, half;
   uint32_t dempty_cl;  // CTA pairs: shared::cluster address of the leader's d_empty[0]
   int o0;              // small images: first output row of the thread (within its image)
+  int vmask;           // window rows 0..2 inside the image (bit I); the others were not computed
+  uint32_t zero_addr;  // TMEM columns [0, D0) of the thread's lane: zeros (full-row bands)
 };
 
 // one tap (compile-time T): three single-row TMEM round trips, D released after the last
@@ -361,17 +381,19 @@ __device__ __forceinline__ void epi_tap(EpiState& e, float (&Y)[RPB][XH], uint64
     }
     return;
   }
+  // window rows outside the image were not computed (band_rows): read the zero columns
+  const int m = e.vmask;
   {  // rows 0 and 1 in flight together: one TMEM round trip instead of two
     float z1[18];
-    issue_row<TW>(a, z);
-    issue_row<TW>(a + Geo<TW>::RS, z1);
+    issue_row<TW>((m & 1) ? a : e.zero_addr, z);
+    issue_row<TW>((m & 2) ? a + Geo<TW>::RS : e.zero_addr, z1);
     tmem_wait_ld();
     finish_row<TW>(e.half, z);
     finish_row<TW>(e.half, z1);
     scatter_row<TW, RPB, CONV, T, 0>(Y, z);
     scatter_row<TW, RPB, CONV, T, 1>(Y, z1);
   }
-  load_row<TW>(a + 2 * Geo<TW>::RS, e.half, z);
+  load_row<TW>((m & 4) ? a + 2 * Geo<TW>::RS : e.zero_addr, e.half, z);
   tc_fence_before();
   __syncwarp();
   if (e.lane == 0) {  // D buffer free: the MMA may refill it (pairs: the leader's barrier)
@@ -407,6 +429,7 @@ __device__ __forceinline__ Work make_work(const TcParams& p) {
 template <int TW, int RPB, int CONV, bool PAIR>
 __device__ void epilogue(const TcParams& p, uint32_t tmem, uint64_t* d_full, uint64_t* d_empty) {
   using G = Geo<TW>;
+  constexpr bool TRIM = !G::STRIP && !G::SMALL && !PAIR;  // see band_rows
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int q = warp % 4;
   const int sub = (warp - EPI_WARP0) / 4;
@@ -416,8 +439,10 @@ __device__ void epilogue(const TcParams& p, uint32_t tmem, uint64_t* d_full, uin
   const int s_img = G::SMALL ? (G::IMGS > 1 ? sub : 0) : 0;
   const int o0 = G::SMALL ? (G::IMGS > 1 ? 0 : sub * G::TR) : 0;
   const uint32_t rb = G::SMALL ? (uint32_t)((s_img * TW + o0) * G::RS) : (uint32_t)(srow * G::RS + half * 16);
-  EpiState e{tmem + ((uint32_t)(q * 32) << 16) + D0 + rb, 0, 0, lane, half,
-             PAIR ? mapa_shared(d_empty, 0) : 0u, o0};
+  EpiState e{tmem + ((uint32_t)(q * 32) << 16) + G::D0 + rb, 0, 0, lane, half,
+             PAIR ? mapa_shared(d_empty, 0) : 0u, o0, 7, tmem + ((uint32_t)(q * 32) << 16) + 1};
+  if constexpr (TRIM) tmem_zero32(tmem + ((uint32_t)(q * 32) << 16));  // every warp of the quadrant
+                                                                        // writes the same zeros
   const int nstrip = G::STRIP ? p.W / 16 : 1;
   float Y[RPB][XH];
   const Work wk = make_work<PAIR>(p);
@@ -447,6 +472,12 @@ __device__ void epilogue(const TcParams& p, uint32_t tmem, uint64_t* d_full, uin
         for (int r = 0; r < RPB; ++r)
 #pragma unroll
           for (int x = 0; x < XH; ++x) Y[r][x] = 0.f;
+        if (TRIM && p.trim) {
+          const int2 v = band_rows<TW>(k, p.H);
+          e.vmask = 0;
+#pragma unroll
+          for (int i = 0; i < 3; ++i) e.vmask |= (srow + i >= v.x && srow + i < v.y) ? 1 << i : 0;
+        }
         epi_tap<TW, RPB, CONV, 0, PAIR>(e, Y, d_full, d_empty);
         epi_tap<TW, RPB, CONV, 1, PAIR>(e, Y, d_full, d_empty);
         epi_tap<TW, RPB, CONV, 2, PAIR>(e, Y, d_full, d_empty);
@@ -486,6 +517,7 @@ struct Ring {
 template <int TW, int RPB, int CONV, bool PAIR>
 __global__ void __launch_bounds__(THREADS, 1) ri_tc_kernel(const __grid_constant__ TcParams p) {
   using G = Geo<TW>;
+  constexpr bool TRIM = !G::STRIP && !G::SMALL && !PAIR;  // see band_rows
   constexpr int NDB = G::NDB;
   constexpr int XTILE = G::XTILE;                     // bytes of a full band tile (global layout)
   constexpr int XS = PAIR ? XTILE / 2 : XTILE;        // bytes of this CTA's part of it in smem
@@ -636,7 +668,17 @@ __global__ void __launch_bounds__(THREADS, 1) ri_tc_kernel(const __grid_constant
     int db = 0;
     uint32_t dph = 0;
     for (int item = wk.first; item < wk.count; item += wk.stride) {
-      for (int k = 0; k < p.NBK; ++k)
+      for (int k = 0; k < p.NBK; ++k) {
+        // full-row bands at the image top / bottom: the halo rows outside the image are zero
+        // padding, so the MMA skips them (N shrinks by RS per row; the epilogue never reads
+        // them, see band_rows)
+        uint32_t idesc_k = idesc, xoff_k = 0, doff_k = 0;
+        if (TRIM && p.trim) {
+          const int2 v = band_rows<TW>(k, p.H);
+          idesc_k = idesc_bf16_f32(128, (uint32_t)((v.y - v.x) * G::RS));
+          xoff_k = (uint32_t)(v.x * G::RS * 128);
+          doff_k = (uint32_t)(v.x * G::RS);
+        }
         for (int b = 0; b < p.NB; ++b) {
           for (int t = 0; t < 9; ++t) {
             if (gd >= NDB) {
@@ -646,7 +688,7 @@ __global__ void __launch_bounds__(THREADS, 1) ri_tc_kernel(const __grid_constant
                 mbar_wait(&d_empty[db], dph ^ 1);
             }
             tc_fence_after();
-            const uint32_t d = tmem + D0 + db * G::MMA_N;
+            const uint32_t d = tmem + G::D0 + db * G::MMA_N + doff_k;
             for (int sp = 0; sp < stages_per_tap; ++sp) {
               if (t == 0 && b == 0 && !p.xstream)
                 for (int cl = 0; cl < p.spc; ++cl) {
@@ -663,31 +705,31 @@ __global__ void __launch_bounds__(THREADS, 1) ri_tc_kernel(const __grid_constant
                   // X chunk: resident band tile c, or the stage's streamed copy
                   const uint32_t xh_a = p.xstream ? wbase + stage_w + cl * XS : xaddr + c * XS;
                   const uint32_t xl_a = p.xstream ? wbase + stage_w + (p.spc + cl) * XS : xaddr + (p.NC + c) * XS;
-                  const uint64_t bh = desc_k_sw128(xh_a);
+                  const uint64_t bh = desc_k_sw128(xh_a + xoff_k);
                   const uint64_t ah = desc_k_sw128(wbase + cl * parts * WTILE);
 #pragma unroll
                   for (int kk = 0; kk < 4; ++kk) {
                     if constexpr (PAIR)
                       mma_bf16_ss_pair(d, ah + 2 * kk, bh + 2 * kk, idesc, (c | kk) != 0);
                     else
-                      mma_bf16_ss(d, ah + 2 * kk, bh + 2 * kk, idesc, (c | kk) != 0);
+                      mma_bf16_ss(d, ah + 2 * kk, bh + 2 * kk, idesc_k, (c | kk) != 0);
                   }
                   if (parts == 2) {
-                    const uint64_t bl = desc_k_sw128(xl_a);
+                    const uint64_t bl = desc_k_sw128(xl_a + xoff_k);
                     const uint64_t al = desc_k_sw128(wbase + (cl * parts + 1) * WTILE);
 #pragma unroll
                     for (int kk = 0; kk < 4; ++kk) {
                       if constexpr (PAIR)
                         mma_bf16_ss_pair(d, ah + 2 * kk, bl + 2 * kk, idesc, 1);
                       else
-                        mma_bf16_ss(d, ah + 2 * kk, bl + 2 * kk, idesc, 1);
+                        mma_bf16_ss(d, ah + 2 * kk, bl + 2 * kk, idesc_k, 1);
                     }
 #pragma unroll
                     for (int kk = 0; kk < 4; ++kk) {
                       if constexpr (PAIR)
                         mma_bf16_ss_pair(d, al + 2 * kk, bh + 2 * kk, idesc, 1);
                       else
-                        mma_bf16_ss(d, al + 2 * kk, bh + 2 * kk, idesc, 1);
+                        mma_bf16_ss(d, al + 2 * kk, bh + 2 * kk, idesc_k, 1);
                     }
                   }
                   if (t == 8 && b == p.NB - 1 && !p.xstream) {  // chunk c of this band fully consumed
@@ -725,6 +767,7 @@ __global__ void __launch_bounds__(THREADS, 1) ri_tc_kernel(const __grid_constant
           }
           if (b == p.NB - 1) ++xc;
         }
+      }
     }
   } else if (warp >= EPI_WARP0) {
     // ------------------------------------------------------------ epilogue
@@ -995,6 +1038,8 @@ int launch_tc(const rc_desc& d, const float* x, const void* bank, const float* b
   {
     const char* ab = getenv("RC_TC_ABLATE");  // profiling switch, see TcParams::ablate
     p.ablate = ab ? atoi(ab) : 0;
+    const char* tr = getenv("RC_TC_TRIM");
+    p.trim = tr ? atoi(tr) : 1;
   }
   int dev, sms;
   RC_CUDA(cudaGetDevice(&dev));

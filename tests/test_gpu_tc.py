@@ -42,6 +42,8 @@ TC_CONFIGS = [
     (2, 256, 16, 256, "p4m", 8, "subgroup", 2, "scatter"),
     (2, 48, 9, 130, "p4m", 8, "subgroup", 1, "raw"),
     (2, 64, 16, 128, "p4m", 8, "avg", 4, "scatter"),
+    (2, 64, 6, 128, "p4m", 8, "max", 8, "scatter"),  # last band: 3 of 6 band rows in the image
+    (1, 64, 2, 128, "p4", 4, "none", 4, "raw"),      # one band, top and bottom rows trimmed
 ]
 
 
