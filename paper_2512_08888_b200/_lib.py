@@ -9,7 +9,8 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "librotconv_b200.so")
+# RC_LIB_VARIANT: a same-box A/B of two builds of this library (tools/gpu_ab_lib.sh)
+LIB_PATH = os.environ.get("RC_LIB_VARIANT") or os.path.join(HERE, "librotconv_b200.so")
 
 RC_OK, RC_ERR_INVALID, RC_ERR_CUDA, RC_ERR_UNSUPPORTED, RC_ERR_WORKSPACE = 0, -1, -2, -3, -4
 GROUPS = {"single": 0, "p4": 1, "p4m": 2, "steer": 3}

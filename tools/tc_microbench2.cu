@@ -286,7 +286,7 @@ __global__ void __launch_bounds__(128, 1)
   } while (0)
 
 template <int N, int MODE>
-void run() {
+void run(int grid = 1) {
   std::vector<__nv_bfloat16> A(128 * 64), B(N * 64);
   std::vector<float> Af(128 * 64), Bf(N * 64);
   srand(N + MODE);
@@ -322,24 +322,39 @@ void run() {
       for (int k = 0; k < 64; ++k) ref += Af[m * 64 + k] * Bf[n * 64 + k];
       if (ref * mult != out[m * N + n]) ++bad;
     }
-  const int iters = 3000;
-  mma_bench<N, MODE><<<1, 128, smem>>>(iters, dA, dB, dout, dcyc);
+  const int iters = grid > 1 ? 30000 : 3000;
+  cudaEvent_t e0, e1;
+  CK(cudaEventCreate(&e0));
+  CK(cudaEventCreate(&e1));
+  CK(cudaEventRecord(e0));
+  mma_bench<N, MODE><<<grid, 128, smem>>>(iters, dA, dB, dout, dcyc);
+  CK(cudaEventRecord(e1));
   CK(cudaDeviceSynchronize());
+  float ms = 0;
+  CK(cudaEventElapsedTime(&ms, e0, e1));
   long long cyc;
   CK(cudaMemcpy(&cyc, dcyc, 8, cudaMemcpyDeviceToHost));
   const int mmas = MODE >= 2 ? (iters / 3) * 12 : iters * 4;
   const double per = (double)cyc / mmas;
   printf("{\"mode\":%d,\"test\":\"%s\",\"M\":128,\"N\":%d,\"correct\":%s,\"mismatches\":%d,\"cycles_per_mma_k16\":%.2f,"
-         "\"macs_per_cycle\":%.1f,\"math_cycles\":%.1f}\n",
+         "\"macs_per_cycle\":%.1f,\"math_cycles\":%.1f,\"grid\":%d,\"ms\":%.4f,\"eff_mhz\":%.0f}\n",
          MODE, MODE == 0 ? "mma_ss" : MODE == 1 ? "mma_ts" : MODE == 2 ? "pattern_bf16x3_ss" : MODE == 3 ? "pattern_bf16x3_whi_tmem" : MODE == 4 ? "pattern_bf16x3_w_tmem" : MODE == 5 ? "kernel_stream_commits" : MODE == 6 ? "kernel_stream_commits_waits" : "commit_ring_depth_x10_plus_chunks_per_stage", N, bad == 0 ? "true" : "false", bad, per,
-         128.0 * N * 16 / per, 128.0 * N * 16 / 4096);
+         128.0 * N * 16 / per, 128.0 * N * 16 / 4096, grid, ms, cyc / (ms * 1e3));
   cudaFree(dA);
   cudaFree(dB);
   cudaFree(dout);
   cudaFree(dcyc);
 }
 
-int main() {
+int main(int argc, char** argv) {
+  if (argc > 1) {  // full-chip runs: clock under sustained tensor load
+    const int g = atoi(argv[1]);
+    run<96, 0>(1);
+    run<96, 0>(g);
+    run<96, 2>(g);
+    run<96, 0>(g);
+    return 0;
+  }
   run<96, 2>();
   run<96, 8>();
   run<112, 2>();
