@@ -264,6 +264,19 @@ __device__ __forceinline__ void tmem_ld2f(uint32_t taddr, float& a, float& b) {
   b = __uint_as_float(r1);
 }
 
+// two consecutive 16-column band rows (TW = 16) in one x32 load: z[1..16], z1[1..16]
+__device__ __forceinline__ void tmem_ld_rows2(uint32_t taddr, float (&z)[18], float (&z1)[18]) {
+  uint32_t r[32];
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];\n"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+               : "r"(taddr));
+#pragma unroll
+  for (int i = 0; i < 16; ++i) {
+    z[1 + i] = __uint_as_float(r[i]);
+    z1[1 + i] = __uint_as_float(r[16 + i]);
+  }
+}
+
 // one input row of the thread's window: 16 columns + (TW = 32, strips) the halo columns.
 // issue_row only issues the TMEM loads; finish_row (after tcgen05.wait::ld) fixes edges.
 template <int TW>
@@ -385,8 +398,12 @@ __device__ __forceinline__ void epi_tap(EpiState& e, float (&Y)[RPB][XH], uint64
   const int m = e.vmask;
   {  // rows 0 and 1 in flight together: one TMEM round trip instead of two
     float z1[18];
-    issue_row<TW>((m & 1) ? a : e.zero_addr, z);
-    issue_row<TW>((m & 2) ? a + Geo<TW>::RS : e.zero_addr, z1);
+    if (TW == 16 && (m & 3) == 3) {
+      tmem_ld_rows2(a, z, z1);
+    } else {
+      issue_row<TW>((m & 1) ? a : e.zero_addr, z);
+      issue_row<TW>((m & 2) ? a + Geo<TW>::RS : e.zero_addr, z1);
+    }
     tmem_wait_ld();
     finish_row<TW>(e.half, z);
     finish_row<TW>(e.half, z1);
