@@ -104,4 +104,9 @@ size_t tc_workspace_bytes(const rc_desc& d);
 int launch_tc_wpack(const rc_desc& d, const float* bases, uint8_t* tc_section, cudaStream_t s);
 int launch_tc(const rc_desc& d, const float* x, const void* bank, const float* bias, float* y, uint8_t* am,
               void* ws, size_t ws_bytes, cudaStream_t s, bool dry_run, const char** name);
+// single-orientation implicit GEMM (ri_igemm.cu), reached through launch_tc
+bool igemm_supported(const rc_desc& d);
+size_t igemm_workspace_bytes(const rc_desc& d);
+int launch_igemm(const rc_desc& d, const float* x, const uint8_t* wpk, const uint8_t* whi, const float* bias,
+                 float* y, uint8_t* am, void* ws, cudaStream_t s);
 }  // namespace rc

@@ -50,6 +50,8 @@ struct Params {
   uint8_t* am;        // [N][Cout][RO][H][W] or null
   int N, Cin, H, Cout, NB, pool, gf, RO, COB, IMG;
   int act;  // rc_activation, applied after the bias
+  int resident;  // small Cin (<= CC): the CTA's images and all weights are loaded into shared
+                 // memory once; the row sweep then runs without copies or CTA barriers
 };
 
 template <int SW, int S, int RPB, int CONV>
@@ -113,14 +115,47 @@ struct SimtK3 {
   // ncl = channels of this chunk (CC, fewer for the last chunk of a small / ragged Cin:
   // the zero-filled tail channels are skipped instead of multiplied)
   __device__ __forceinline__ void compute_stage(const float* st, int ncl) {
-    const float* sx = st + img_l * CC * W + x0;
-    const float4* sw = reinterpret_cast<const float4*>(st + stage_x) + co_l * 3;
+    compute_rows(st + img_l * CC * W + x0, W, reinterpret_cast<const float4*>(st + stage_x) + co_l * 3, ncl);
+  }
+  // resident mode: X [img][ci][H][W], then weights [b][ci][COB][12] for all bases
+  __device__ __forceinline__ void compute_resident(int b, int q) {
+    const float* sx = smem + ((size_t)img_l * p.Cin * p.H + q) * W + x0;
+    const float* swf = smem + (size_t)p.IMG * p.Cin * p.H * W;
+    compute_rows(sx, p.H * W, reinterpret_cast<const float4*>(swf) + ((size_t)b * p.Cin * p.COB + co_l) * 3, p.Cin);
+  }
+  __device__ void load_resident() {
+    const int xq = W / 4;
+    const int per_img = p.Cin * p.H * xq;
+    const int n0 = blockIdx.y * p.IMG;
+    for (int i = tid; i < p.IMG * per_img; i += blockDim.x) {
+      const int img = i / per_img, rem = i % per_img;
+      const bool ok = n0 + img < p.N;
+      cp_async16(smem + (size_t)i * 4, p.x + ((size_t)(ok ? n0 + img : 0) * per_img + rem) * 4, ok);
+    }
+    float* sw = smem + (size_t)p.IMG * p.Cin * p.H * W;
+    const int nw = p.NB * p.Cin * p.COB * 3;
+    const int co0 = blockIdx.x * p.COB;
+    for (int i = tid; i < nw; i += blockDim.x) {
+      const int b = i / (p.Cin * p.COB * 3), r1 = i % (p.Cin * p.COB * 3);
+      const int ci = r1 / (p.COB * 3), r2 = r1 % (p.COB * 3);
+      const int cc = r2 / 3, part = r2 % 3;
+      const bool ok = co0 + cc < p.Cout;
+      const float* src = p.wk + ((((size_t)b * p.Cin + ci) * p.Cout + (ok ? co0 + cc : 0)) * 12 + part * 4);
+      cp_async16(sw + (size_t)i * 4, src, ok);
+    }
+    cp_async_commit();
+    cp_async_wait<0>();
+    __syncthreads();
+  }
+  // channel dots of ncl channels (channel stride cs floats; weights 3 float4 per channel,
+  // COB*3 float4 apart), accumulated in ascending ci
+  __device__ __forceinline__ void compute_rows(const float* sx, int cs, const float4* sw, int ncl) {
 #pragma unroll 4
     for (int cl = 0; cl < ncl; ++cl) {
       float xv[SW];
 #pragma unroll
       for (int v = 0; v < SW / 4; ++v) {
-        const float4 t4 = *reinterpret_cast<const float4*>(sx + cl * W + v * 4);
+        const float4 t4 = *reinterpret_cast<const float4*>(sx + (size_t)cl * cs + v * 4);
         xv[v * 4 + 0] = t4.x;
         xv[v * 4 + 1] = t4.y;
         xv[v * 4 + 2] = t4.z;
@@ -253,7 +288,9 @@ struct SimtK3 {
     for (int t = 0; t < 9; ++t)
 #pragma unroll
       for (int j = 0; j < SW; ++j) Z[t][j] = 0.f;
-    if (q < p.H) {
+    if (q < p.H && p.resident) {
+      compute_resident(b, q);
+    } else if (q < p.H) {
       for (int c = 0; c < nchunks; ++c, ++gi) {
         issue(gi + 1, total);
         cp_async_wait<1>();
@@ -301,7 +338,10 @@ struct SimtK3 {
   __device__ void run() {
     const int total = p.NB * p.H * nchunks;
     int gi = 0;
-    issue(0, total);
+    if (p.resident)
+      load_resident();
+    else
+      issue(0, total);
     for (int b = 0; b < p.NB; ++b) {
       for (int q0 = 0; q0 <= p.H; q0 += 3) {
         step<0>(b, q0, gi, total);
@@ -395,7 +435,11 @@ int launch_simt_k3(const rc_desc& d, const float* x, const void* bank, const flo
   p.COB = COB;
   p.IMG = IMG;
   p.act = d.activation;
-  const size_t smem = 2 * sizeof(float) * ((size_t)IMG * CC * d.w + (size_t)CC * COB * 12);
+  size_t smem = 2 * sizeof(float) * ((size_t)IMG * CC * d.w + (size_t)CC * COB * 12);
+  const size_t smem_res = sizeof(float) * ((size_t)IMG * d.c_in * d.h * d.w + (size_t)p.NB * d.c_in * COB * 12);
+  const char* re = getenv("RC_SIMT_RESIDENT");  // A/B switch (default on)
+  p.resident = (re ? atoi(re) : 1) && d.c_in <= CC && smem_res <= 200 * 1024;
+  if (p.resident) smem = std::max(smem, smem_res);
   const int gx = (d.c_out + COB - 1) / COB, gy = (d.n + IMG - 1) / IMG;
   if (gy > 65535) return RC_ERR_UNSUPPORTED;
   if (SW == 4) {

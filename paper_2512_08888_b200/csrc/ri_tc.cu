@@ -956,7 +956,8 @@ SmemPlan smem_plan(const TcGeom& g, int parts, bool pair = false) {
 
 }  // namespace
 
-bool tc_supported(const rc_desc& d) {
+namespace {
+bool band_supported(const rc_desc& d) {
   const int gf = pool_fold(d);
   const int R = d.orientations;
   const bool fold_ok = d.pool == RC_POOL_NONE || (d.pool == RC_POOL_AVG && (R & (R - 1)) == 0) || gf == 1 ||
@@ -969,12 +970,17 @@ bool tc_supported(const rc_desc& d) {
   const int parts = d.precision == RC_PREC_BF16 ? 1 : 2;
   return smem_plan(geom(d), parts).spc > 0;
 }
+}  // namespace
+
+// single orientation: implicit GEMM (ri_igemm.cu); otherwise the band kernels of this file
+bool tc_supported(const rc_desc& d) { return igemm_supported(d) || band_supported(d); }
 size_t tc_bank_bytes(const rc_desc& d) {
   if (d.k != 3) return 0;
   return 3 * geom(d).w_plane;  // interleaved hi/lo + hi-only
 }
 size_t tc_workspace_bytes(const rc_desc& d) {
-  if (!tc_supported(d)) return 0;
+  if (igemm_supported(d)) return igemm_workspace_bytes(d);
+  if (!band_supported(d)) return 0;
   return 2 * geom(d).x_plane;
 }
 
@@ -991,7 +997,15 @@ int launch_tc_wpack(const rc_desc& d, const float* bases, uint8_t* tc_section, c
 
 int launch_tc(const rc_desc& d, const float* x, const void* bank, const float* bias, float* y, uint8_t* am,
               void* ws, size_t ws_bytes, cudaStream_t s, bool dry_run, const char** name) {
-  if (!tc_supported(d)) return RC_ERR_UNSUPPORTED;
+  if (igemm_supported(d)) {
+    if (name) *name = d.precision == RC_PREC_BF16 ? "tc_igemm_bf16" : "tc_igemm_bf16x3";
+    if (dry_run || d.n == 0) return RC_OK;
+    if (ws_bytes < igemm_workspace_bytes(d) || ws == nullptr)
+      return fail(RC_ERR_WORKSPACE, "ri_conv: workspace too small for the tensor-core path");
+    const uint8_t* tcb = static_cast<const uint8_t*>(bank) + bank_layout(d).tc_off;
+    return launch_igemm(d, x, tcb, tcb + 2 * geom(d).w_plane, bias, y, am, ws, s);
+  }
+  if (!band_supported(d)) return RC_ERR_UNSUPPORTED;
   if (name) {
     static const char* names[5][2] = {{"tc_k3w16_bf16x3", "tc_k3w16_bf16"},
                                       {"tc_k3w32_bf16x3", "tc_k3w32_bf16"},

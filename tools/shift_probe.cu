@@ -1,0 +1,96 @@
+// shift_probe.cu -- can a tcgen05 SW128 K-major operand start at an arbitrary 128-byte row
+// of a 1024-byte-aligned swizzled tile?  (implicit-GEMM convolution: a tap = a row shift)
+// A: 256 rows x 64 K (bf16) in SW128 K-major; B: 64 rows x 64 K.  For each shift s the MMA
+// uses A rows s .. s+127 (descriptor start = base + 128*s, with the matrix base-offset field
+// 0 or (s & 7)) and D is compared with the CPU product.  One JSON line per (s, mode).
+// Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -I../paper_2512_08888_b200/csrc
+#include <cuda_bf16.h>
+
+#include <cstdio>
+#include <vector>
+
+#include "tc_ptx.cuh"
+
+using namespace rc::tc;
+
+constexpr int AR = 256, N = 64;
+
+__global__ void __launch_bounds__(128, 1)
+    probe(int s, int mode, const __nv_bfloat16* Ag, const __nv_bfloat16* Bg, float* out) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  __nv_bfloat16* sA = reinterpret_cast<__nv_bfloat16*>(smem);
+  __nv_bfloat16* sB = reinterpret_cast<__nv_bfloat16*>(smem + AR * 128);
+  __shared__ uint64_t bar;
+  __shared__ uint32_t tbase;
+  const int tid = threadIdx.x, warp = tid / 32;
+  for (int i = tid; i < AR * 64; i += blockDim.x) sA[sw128_offset(i / 64, i % 64) / 2] = Ag[i];
+  for (int i = tid; i < N * 64; i += blockDim.x) sB[sw128_offset(i / 64, i % 64) / 2] = Bg[i];
+  fence_proxy_async_smem();
+  if (warp == 0) tmem_alloc<512>(&tbase);
+  if (tid == 0) {
+    mbar_init(&bar, 1);
+    fence_barrier_init();
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (tid == 0) {
+    uint64_t da = desc_k_sw128(smem_u32(sA) + 128 * s);
+    if (mode == 1) da |= (uint64_t)(s & 7) << 49;
+    const uint64_t db = desc_k_sw128(smem_u32(sB));
+    const uint32_t idesc = idesc_bf16_f32(128, N);
+    for (int kk = 0; kk < 4; ++kk) mma_bf16_ss(tbase, da + 2 * kk, db + 2 * kk, idesc, kk != 0);
+    mma_commit(&bar);
+  }
+  mbar_wait(&bar, 0);
+  tc_fence_after();
+  float v[32];
+  for (int c = 0; c < N; c += 32) {
+    tmem_ld32(tbase + ((uint32_t)(warp * 32) << 16) + c, v);
+    tmem_wait_ld();
+    for (int j = 0; j < 32; ++j) out[tid * N + c + j] = v[j];
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) tmem_dealloc<512>(tbase);
+}
+
+int main() {
+  std::vector<__nv_bfloat16> A(AR * 64), B(N * 64);
+  std::vector<float> Af(AR * 64), Bf(N * 64);
+  srand(1);
+  for (int i = 0; i < AR * 64; ++i) A[i] = __float2bfloat16(Af[i] = (float)(rand() % 9 - 4));
+  for (int i = 0; i < N * 64; ++i) B[i] = __float2bfloat16(Bf[i] = (float)(rand() % 9 - 4));
+  __nv_bfloat16 *dA, *dB;
+  float* dout;
+  cudaMalloc(&dA, A.size() * 2);
+  cudaMalloc(&dB, B.size() * 2);
+  cudaMalloc(&dout, 128 * N * 4);
+  cudaMemcpy(dA, A.data(), A.size() * 2, cudaMemcpyHostToDevice);
+  cudaMemcpy(dB, B.data(), B.size() * 2, cudaMemcpyHostToDevice);
+  const int smem = AR * 128 + N * 128 + 2048;
+  cudaFuncSetAttribute(probe, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  std::vector<float> out(128 * N);
+  const int shifts[] = {0, 1, 2, 3, 5, 7, 8, 9, 13, 18, 34, 66, 127};
+  for (int s : shifts)
+    for (int mode = 0; mode < 2; ++mode) {
+      probe<<<1, 128, smem>>>(s, mode, dA, dB, dout);
+      cudaError_t e = cudaDeviceSynchronize();
+      if (e != cudaSuccess) {
+        printf("{\"shift\":%d,\"mode\":%d,\"error\":\"%s\"}\n", s, mode, cudaGetErrorString(e));
+        return 1;
+      }
+      cudaMemcpy(out.data(), dout, out.size() * 4, cudaMemcpyDeviceToHost);
+      int bad = 0, bad_vs_unshifted_rows = 0;
+      for (int m = 0; m < 128; ++m)
+        for (int n = 0; n < N; ++n) {
+          float ref = 0;
+          for (int k = 0; k < 64; ++k) ref += Af[(s + m) * 64 + k] * Bf[n * 64 + k];
+          if (ref != out[m * N + n]) ++bad;
+        }
+      (void)bad_vs_unshifted_rows;
+      printf("{\"shift\":%d,\"mode\":%d,\"mismatches\":%d}\n", s, mode, bad);
+    }
+  return 0;
+}
