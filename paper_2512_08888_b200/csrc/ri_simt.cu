@@ -57,8 +57,12 @@ struct Params {
 template <int SW, int S, int RPB, int CONV>
 struct SimtK3 {
   static constexpr int W = SW * S;
-  float Z[9][SW];
-  float Y[3][RPB][SW];
+  // register pairs: the channel dots and the scatter run as packed FP32x2 (FFMA2 / FADD2,
+  // one instruction per two columns; per-lane IEEE fma / add, so results are unchanged)
+  float2 Z2[9][SW / 2];
+  float2 Y2[3][RPB][SW / 2];
+  __device__ __forceinline__ float& Y(int s, int r, int j) { return (j & 1) ? Y2[s][r][j >> 1].y : Y2[s][r][j >> 1].x; }
+  __device__ __forceinline__ float& Z(int t, int j) { return (j & 1) ? Z2[t][j >> 1].y : Z2[t][j >> 1].x; }
 
   const Params& p;
   float* smem;
@@ -166,9 +170,12 @@ struct SimtK3 {
       const float4 cq = sw[cl * p.COB * 3 + 2];
       const float wv[9] = {a.x, a.y, a.z, a.w, bq.x, bq.y, bq.z, bq.w, cq.x};
 #pragma unroll
-      for (int t = 0; t < 9; ++t)
+      for (int t = 0; t < 9; ++t) {
+        const float2 w2 = make_float2(wv[t], wv[t]);
 #pragma unroll
-        for (int j = 0; j < SW; ++j) Z[t][j] = fmaf(wv[t], xv[j], Z[t][j]);
+        for (int k = 0; k < SW / 2; ++k)
+          Z2[t][k] = __ffma2_rn(w2, make_float2(xv[2 * k], xv[2 * k + 1]), Z2[t][k]);
+      }
     }
   }
 
@@ -203,7 +210,7 @@ struct SimtK3 {
       for (int r = 0; r < RPB; ++r) {
         float v[SW];
 #pragma unroll
-        for (int j = 0; j < SW; ++j) v[j] = activate(Y[SLOT][r][j] + bz);
+        for (int j = 0; j < SW; ++j) v[j] = activate(Y(SLOT, r, j) + bz);
         store_vec(p.y + ybase + (size_t)(b * RPB + r) * plane, v);
       }
       return;
@@ -212,15 +219,15 @@ struct SimtK3 {
       float acc[SW];
       if (b == 0) {
 #pragma unroll
-        for (int j = 0; j < SW; ++j) acc[j] = Y[SLOT][0][j];
+        for (int j = 0; j < SW; ++j) acc[j] = Y(SLOT, 0, j);
       } else {
 #pragma unroll
-        for (int j = 0; j < SW; ++j) acc[j] = p.y[ybase + j] + Y[SLOT][0][j];
+        for (int j = 0; j < SW; ++j) acc[j] = p.y[ybase + j] + Y(SLOT, 0, j);
       }
 #pragma unroll
       for (int r = 1; r < RPB; ++r)
 #pragma unroll
-        for (int j = 0; j < SW; ++j) acc[j] += Y[SLOT][r][j];
+        for (int j = 0; j < SW; ++j) acc[j] += Y(SLOT, r, j);
       if (b == p.NB - 1) {
 #pragma unroll
         for (int j = 0; j < SW; ++j) acc[j] = activate(acc[j] / (float)R + bz);
@@ -240,7 +247,7 @@ struct SimtK3 {
       if (kk == 0) {
 #pragma unroll
         for (int j = 0; j < SW; ++j) {
-          best[j] = Y[SLOT][r][j];
+          best[j] = Y(SLOT, r, j);
           arg[j] = 0;
         }
       } else {
@@ -253,8 +260,8 @@ struct SimtK3 {
         }
 #pragma unroll
         for (int j = 0; j < SW; ++j)
-          if (Y[SLOT][r][j] > best[j]) {
-            best[j] = Y[SLOT][r][j];
+          if (Y(SLOT, r, j) > best[j]) {
+            best[j] = Y(SLOT, r, j);
             arg[j] = (uint8_t)kk;
           }
       }
@@ -277,17 +284,17 @@ struct SimtK3 {
 #pragma unroll
     for (int r = 0; r < RPB; ++r)
 #pragma unroll
-      for (int j = 0; j < SW; ++j) Y[(P + 1) % 3][r][j] = 0.f;
+      for (int k = 0; k < SW / 2; ++k) Y2[(P + 1) % 3][r][k] = make_float2(0.f, 0.f);
     if (P == 0 && q == 0) {
 #pragma unroll
       for (int r = 0; r < RPB; ++r)
 #pragma unroll
-        for (int j = 0; j < SW; ++j) Y[0][r][j] = 0.f;
+        for (int k = 0; k < SW / 2; ++k) Y2[0][r][k] = make_float2(0.f, 0.f);
     }
 #pragma unroll
     for (int t = 0; t < 9; ++t)
 #pragma unroll
-      for (int j = 0; j < SW; ++j) Z[t][j] = 0.f;
+      for (int k = 0; k < SW / 2; ++k) Z2[t][k] = make_float2(0.f, 0.f);
     if (q < p.H && p.resident) {
       compute_resident(b, q);
     } else if (q < p.H) {
@@ -304,8 +311,8 @@ struct SimtK3 {
 #pragma unroll
     for (int t = 0; t < 9; ++t) {
       if constexpr (S > 1) {
-        const float l = __shfl_up_sync(0xffffffffu, Z[t][SW - 1], 1, S);
-        const float rr = __shfl_down_sync(0xffffffffu, Z[t][0], 1, S);
+        const float l = __shfl_up_sync(0xffffffffu, Z2[t][SW / 2 - 1].y, 1, S);
+        const float rr = __shfl_down_sync(0xffffffffu, Z2[t][0].x, 1, S);
         Zl[t] = seg == 0 ? 0.f : l;
         Zr[t] = seg == S - 1 ? 0.f : rr;
       } else {
@@ -313,25 +320,30 @@ struct SimtK3 {
         Zr[t] = 0.f;
       }
     }
-    // reuse scatter: each Z_t feeds all RPB rotations (PAPER Eq. 8)
+    // reuse scatter: each Z_t feeds all RPB rotations (PAPER Eq. 8).
+    // Y[j] += Z[j + dj]: dj = 0 adds the aligned pairs Z2[k]; dj = -1 / +1 add the odd-aligned
+    // pairs B[k] = (Z[2k-1], Z[2k]) / B[k+1], built once per tap (halo columns included).
     constexpr K3Tables TB = make_k3(CONV);
 #pragma unroll
-    for (int t = 0; t < 9; ++t)
+    for (int t = 0; t < 9; ++t) {
+      float2 B[SW / 2 + 1];
+      B[0] = make_float2(Zl[t], Z2[t][0].x);
+#pragma unroll
+      for (int k = 1; k < SW / 2; ++k) B[k] = make_float2(Z2[t][k - 1].y, Z2[t][k].x);
+      B[SW / 2] = make_float2(Z2[t][SW / 2 - 1].y, Zr[t]);
 #pragma unroll
       for (int r = 0; r < RPB; ++r) {
-        constexpr int dummy = 0;
-        (void)dummy;
         const int di = TB.di[r][t], dj = TB.dj[r][t];
         const int slot = (P - di + 3) % 3;
 #pragma unroll
-        for (int j = 0; j < SW; ++j) {
-          const int src = j + dj;
-          const float v = src < 0 ? Zl[t] : (src >= SW ? Zr[t] : Z[t][src < 0 ? 0 : (src >= SW ? SW - 1 : src)]);
-          if (slot == 0) Y[0][r][j] += v;
-          else if (slot == 1) Y[1][r][j] += v;
-          else Y[2][r][j] += v;
+        for (int k = 0; k < SW / 2; ++k) {
+          const float2 v = dj == 0 ? Z2[t][k] : (dj < 0 ? B[k] : B[k + 1]);
+          if (slot == 0) Y2[0][r][k] = __fadd2_rn(Y2[0][r][k], v);
+          else if (slot == 1) Y2[1][r][k] = __fadd2_rn(Y2[1][r][k], v);
+          else Y2[2][r][k] = __fadd2_rn(Y2[2][r][k], v);
         }
       }
+    }
     if (q >= 1) finalize<(P + 2) % 3>(b, q - 1);
   }
 
