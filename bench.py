@@ -69,18 +69,36 @@ def peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled DURING the timed region."""
+    """SM clock + throttle reasons sampled DURING the timed region: NVML polled every 2 ms
+    from a thread, plus explicit sample() calls while queued GPU work is still running (a
+    sub-millisecond timed region still gets samples).  Falls back to nvidia-smi -lms 10."""
 
     Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
          "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
          "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    NAMES = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
 
     def __init__(self, index: int):
         self.index = index
         self.proc = None
+        self.nvml = None
+        self.rows: list = []
         self.lines: list[str] = []
+        self.stop = threading.Event()
 
     def __enter__(self):
+        try:
+            import pynvml as N
+            N.nvmlInit()
+            vis = os.environ.get("CUDA_VISIBLE_DEVICES")
+            phys = int(vis.split(",")[self.index]) if vis and vis.split(",")[0].isdigit() else self.index
+            self.h = N.nvmlDeviceGetHandleByIndex(phys)
+            self.nvml = N
+            self.t = threading.Thread(target=self._poll, daemon=True)
+            self.t.start()
+            return self
+        except Exception:
+            self.nvml = None
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
@@ -92,11 +110,32 @@ class ClockSampler:
             self.proc = None
         return self
 
+    def sample(self):
+        if self.nvml is None:
+            return
+        N = self.nvml
+        try:
+            sm = N.nvmlDeviceGetClockInfo(self.h, N.NVML_CLOCK_SM)
+            mx = N.nvmlDeviceGetMaxClockInfo(self.h, N.NVML_CLOCK_SM)
+            r = N.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+            bits = [0x8, 0x40, 0x20, 0x4]  # hw_slowdown, hw_thermal, sw_thermal, sw_power_cap
+            self.rows.append((float(sm), float(mx), ["Active" if r & b else "Not Active" for b in bits]))
+        except Exception:
+            pass
+
+    def _poll(self):
+        while not self.stop.is_set():
+            self.sample()
+            time.sleep(0.002)
+
     def _read(self):
         for line in self.proc.stdout:
             self.lines.append(line.strip())
 
     def __exit__(self, *a):
+        self.stop.set()
+        if self.nvml is not None:
+            self.t.join(timeout=1)
         if self.proc:
             self.proc.terminate()
             try:
@@ -105,7 +144,7 @@ class ClockSampler:
                 self.proc.kill()
 
     def summary(self):
-        rows = []
+        rows = list(self.rows)
         for l in self.lines:
             f = [x.strip() for x in l.split(",")]
             if len(f) >= 9:
@@ -115,10 +154,10 @@ class ClockSampler:
                     pass
         if not rows:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for _, _, fl in rows for i, v in enumerate(fl) if v.lower() == "active"})
+        reasons = sorted({self.NAMES[i] for _, _, fl in rows for i, v in enumerate(fl) if v.lower() == "active"})
         return {"sm_mhz": statistics.median(r[0] for r in rows), "sm_max_mhz": max(r[1] for r in rows),
-                "reasons": reasons, "samples": len(rows)}
+                "reasons": reasons, "samples": len(rows),
+                "source": "nvml" if self.nvml is not None else "nvidia-smi"}
 
 
 def cpu_reference(wl, threads: int, target_s: float = 12.0):
@@ -287,6 +326,7 @@ def run_stack(args, wl):
             ev[i][0].record(stream)
             stack.graph_forward(x)
             ev[i][1].record(stream)
+        clk.sample()  # the queued steps are still running on the GPU
         torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
@@ -444,6 +484,7 @@ def main():
             ev[i][0].record(stream)
             step()
             ev[i][1].record(stream)
+        clk.sample()  # the queued steps are still running on the GPU
         torch.cuda.synchronize()
     L.rc_profile_enable(0)
     kms = (C.c_float * args.steps)()
