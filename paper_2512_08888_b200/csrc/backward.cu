@@ -184,8 +184,9 @@ size_t bwd_input_ws(const rc_desc& d) {
 
 size_t bwd_weight_ws(const rc_desc& d) {
   const int R = num_bases(d) * rot_per_base(d);
-  const size_t cols = (size_t)d.h * d.w * d.c_in * d.k * d.k * sizeof(float);
   const size_t dF = (size_t)d.c_out * R * d.c_in * d.k * d.k * sizeof(float);
+  if (wgrad_supported(d)) return align256(dF) + wgrad_ws_bytes(d);  // tensor-core implicit GEMM
+  const size_t cols = (size_t)d.h * d.w * d.c_in * d.k * d.k * sizeof(float);
   return align256(cols) + align256(dF);
 }
 
@@ -218,9 +219,18 @@ int launch_bwd_input(const rc_desc& d, const float* df, const void* bank, float*
   return dispatch_forward(sd, df, sbank, nullptr, dx, nullptr, sws, tc_workspace_bytes(sd), s);
 }
 
+static int param_grad(const rc_desc& d, const float* dF, float* dw0, float* dw1, cudaStream_t s);
+
 int launch_bwd_weight(const rc_desc& d, const float* x, const float* df, float* dw0, float* dw1, void* ws,
                       cudaStream_t s) {
   const int R = num_bases(d) * rot_per_base(d), KK = d.k * d.k;
+  if (wgrad_supported(d)) {  // bf16 / bf16x3 / auto: one tcgen05 implicit GEMM over the batch
+    float* dF = static_cast<float*>(ws);
+    const size_t dFb = align256((size_t)d.c_out * R * d.c_in * KK * sizeof(float));
+    const int st = launch_wgrad(d, x, df, dF, static_cast<char*>(ws) + dFb, s);
+    if (st != RC_OK) return st;
+    return param_grad(d, dF, dw0, dw1, s);
+  }
   const size_t colsb = align256((size_t)d.h * d.w * d.c_in * KK * sizeof(float));
   float* cols = static_cast<float*>(ws);
   float* dF = reinterpret_cast<float*>(static_cast<char*>(ws) + colsb);
@@ -249,6 +259,12 @@ int launch_bwd_weight(const rc_desc& d, const float* x, const float* df, float* 
                                           df + (size_t)n * M * plane, Kd, &one, dF, Ncol);
     if (cs != CUBLAS_STATUS_SUCCESS) return fail(RC_ERR_CUDA, "ri_conv_backward: cublasSgemm failed");
   }
+  return param_grad(d, dF, dw0, dw1, s);
+}
+
+// dF -> parameter gradients: inverse rotations (Eq. 16) and the mirror / steer chain rule
+static int param_grad(const rc_desc& d, const float* dF, float* dw0, float* dw1, cudaStream_t s) {
+  const int KK = d.k * d.k;
   TapOffsets T;
   slice_tap_offsets(d.k, d.convention, &T);
   SteerCo sc{};

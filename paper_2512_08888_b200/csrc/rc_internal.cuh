@@ -109,4 +109,17 @@ bool igemm_supported(const rc_desc& d);
 size_t igemm_workspace_bytes(const rc_desc& d);
 int launch_igemm(const rc_desc& d, const float* x, const uint8_t* wpk, const uint8_t* whi, const float* bias,
                  float* y, uint8_t* am, void* ws, cudaStream_t s);
+// zero-padded pixel-row planes of X (ri_igemm.cu): plane c = [rows][64 ci] bf16 SW128 rows,
+// row G + q for padded pixel q = n*Pimg + (h+1)*Wp + (w+1); hi and (xl != null) lo parts
+struct PadGeom {
+  int Wp, G, Pimg, NC;
+  long long rows;
+};
+PadGeom pad_geom(const rc_desc& d);
+size_t pad_planes_bytes(const rc_desc& d, int parts);
+int launch_pad_pack(const rc_desc& d, const float* x, uint8_t* xh, uint8_t* xl, cudaStream_t s);
+// weight gradient on the tensor cores (ri_wgrad.cu): dF[m][ci*9 + pos] for K = 3
+bool wgrad_supported(const rc_desc& d);
+size_t wgrad_ws_bytes(const rc_desc& d);
+int launch_wgrad(const rc_desc& d, const float* x, const float* df, float* dF, void* ws, cudaStream_t s);
 }  // namespace rc

@@ -352,6 +352,25 @@ size_t igemm_workspace_bytes(const rc_desc& d) {
   return (size_t)parts * g.NC * g.rows * 128;
 }
 
+PadGeom pad_geom(const rc_desc& d) {
+  const IgGeom g = ig_geom(d);
+  return PadGeom{g.Wp, g.G, g.Pimg, g.NC, g.rows};
+}
+
+size_t pad_planes_bytes(const rc_desc& d, int parts) {
+  const IgGeom g = ig_geom(d);
+  return (size_t)parts * g.NC * g.rows * 128;
+}
+
+int launch_pad_pack(const rc_desc& d, const float* x, uint8_t* xh, uint8_t* xl, cudaStream_t s) {
+  const IgGeom g = ig_geom(d);
+  const long long total = (long long)g.NC * ((g.rows + PACK_ROWS - 1) / PACK_ROWS);
+  const long long grid = total < 148 * 16 ? total : 148 * 16;
+  ig_pack_kernel<<<(int)grid, 256, 0, s>>>(x, xh, xl, d.n, d.c_in, d.h, d.w, g.Wp, g.G, g.Pimg, g.rows, g.NC);
+  RC_CUDA(cudaGetLastError());
+  return RC_OK;
+}
+
 // bank: the tc section of the bank (ri_tc.cu's packed weights; whi = its hi-only plane)
 int launch_igemm(const rc_desc& d, const float* x, const uint8_t* wpk, const uint8_t* whi, const float* bias,
                  float* y, uint8_t* am, void* ws, cudaStream_t s) {
@@ -362,10 +381,8 @@ int launch_igemm(const rc_desc& d, const float* x, const uint8_t* wpk, const uin
   uint8_t* xh = static_cast<uint8_t*>(ws);
   uint8_t* xl = parts == 2 ? xh + (size_t)g.NC * g.rows * 128 : nullptr;
   {
-    const long long total = (long long)g.NC * ((g.rows + PACK_ROWS - 1) / PACK_ROWS);
-    const long long grid = total < 148 * 16 ? total : 148 * 16;
-    ig_pack_kernel<<<(int)grid, 256, 0, s>>>(x, xh, xl, d.n, d.c_in, d.h, d.w, g.Wp, g.G, g.Pimg, g.rows, g.NC);
-    RC_CUDA(cudaGetLastError());
+    const int st = launch_pad_pack(d, x, xh, xl, s);
+    if (st != RC_OK) return st;
   }
   IgParams p;
   p.xh = xh;
