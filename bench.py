@@ -219,6 +219,28 @@ def run_reference(args, wl):
     print(json.dumps(out), flush=True)
 
 
+def backward_context(P, desc, x, bank, y, am, reps=3):
+    """The layer's backward (SPEC backward module: pool/ReLU/bias backward, input gradient,
+    weight gradient) on the same inputs, CUDA-event timed after one warm-up; context for the
+    forward line, not part of the timed step."""
+    import torch
+    gy = torch.rand(y.shape, device=x.device)
+    run = lambda: P.ri_conv_backward(desc, x, bank, gy, y, am)
+    run()
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    for _ in range(reps):
+        run()
+    b.record()
+    b.synchronize()
+    ms = a.elapsed_time(b) / reps
+    return {"ms": ms,
+            "grads": "dx, dW (f_x, f_y for steer), dbias",
+            "path": "rc_ri_conv_backward: pool backward, implicit-GEMM input gradient, tcgen05 weight gradient"
+            if desc.kernel_name().startswith("tc_") else "rc_ri_conv_backward (fp32: CUDA-core input pass, SGEMM weights)"}
+
+
 def cudnn_context(P, desc, x, fx, fy, ours_ms, args):
     """Context only (not the product path): the same R orientation slices
     as R separate cuDNN convolutions on the rotated kernels (the paper's cuDNN RI pipeline),
@@ -424,6 +446,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-cudnn", action="store_true", help="skip the cuDNN context measurement")
+    ap.add_argument("--no-backward", action="store_true", help="skip the layer-backward context measurement")
     args = ap.parse_args()
     wl = WORKLOADS[args.workload]
     if args.impl == "reference":
@@ -539,6 +562,9 @@ def main():
     cudnn_ctx = None
     if rank == 0 and world == 1 and not args.no_cudnn:
         cudnn_ctx = cudnn_context(P, desc, x, fx, fy, ms, args)
+    bwd = None
+    if rank == 0 and world == 1 and not args.no_backward:
+        bwd = backward_context(P, desc, x, bank, y, am)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         v, info = cpu_reference(wl, os.cpu_count() or 1)
@@ -577,6 +603,7 @@ def main():
             "gpu_launches_note": "per step: tc path = x_pack_kernel + ri_tc_kernel; SIMT = one fused kernel",
             "cpu_baseline": cpu,
             "cudnn_context": cudnn_ctx,
+            "backward_context": bwd,
             "timed_output_matches_e2e": bool(ok),
         }
         print(json.dumps(out), flush=True)

@@ -52,6 +52,7 @@ struct IgParams {
   int N, H, W, Cout, NC, NCTW, NN, NCTN, tiles, items;
   int Wp, G, Pimg, xrows, parts, passes, x_stages, w_stages, act;
   int off[9];         // A row shift of base tap t
+  int seg;            // ci chunks per TMEM accumulation segment
 };
 
 __device__ __forceinline__ void split_bf16(float v, __nv_bfloat16& hi, __nv_bfloat16& lo) {
@@ -203,10 +204,14 @@ __global__ void __launch_bounds__(THREADS, 1) igemm_kernel(const __grid_constant
       const long long q0 = (long long)tile * 128;
       const long long r0 = ((long long)p.G + q0 - p.Wp - 1) & ~7LL;
       const uint32_t arow0 = (uint32_t)(p.G + q0 - r0);  // A row of pixel q0 in the X stage
-      if (gd >= 2) mbar_wait(&d_empty[db], dph ^ 1);
-      tc_fence_after();
-      const uint32_t d = tmem + db * p.NN;
+      uint32_t d = 0;
       for (int c = 0; c < p.NC; ++c) {
+        if (c % p.seg == 0) {  // a new accumulation segment: the next D buffer
+          if (gd >= 2) mbar_wait(&d_empty[db], dph ^ 1);
+          tc_fence_after();
+          d = tmem + db * p.NN;
+        }
+        const bool seg_end = c % p.seg == p.seg - 1 || c == p.NC - 1;
         mbar_wait(&x_full[xr.s], xr.ph);
         const uint32_t xa = smem_u32(xs + xr.s * xstage);
         for (int t = 0; t < 9; ++t) {
@@ -216,7 +221,7 @@ __global__ void __launch_bounds__(THREADS, 1) igemm_kernel(const __grid_constant
             const uint32_t wa = smem_u32(ws + wr.s * wstage);
             const uint32_t arow = (arow0 + p.off[t]) * 128;
             const uint64_t ah = desc_k_sw128(xa + arow), bh = desc_k_sw128(wa);
-            const uint32_t acc = (c | t) != 0;
+            const uint32_t acc = (c % p.seg != 0) || t != 0;
 #pragma unroll
             for (int kk = 0; kk < 4; ++kk) mma_bf16_ss(d, ah + 2 * kk, bh + 2 * kk, idesc, acc | kk);
             if (p.passes == 3) {
@@ -228,17 +233,19 @@ __global__ void __launch_bounds__(THREADS, 1) igemm_kernel(const __grid_constant
             }
             mma_commit(&w_empty[wr.s]);
             if (t == 8) mma_commit(&x_empty[xr.s]);
-            if (t == 8 && c == p.NC - 1) mma_commit(&d_full[db]);
+            if (t == 8 && seg_end) mma_commit(&d_full[db]);
           }
           __syncwarp();
           wr.adv(S);
         }
         xr.adv(p.x_stages);
-      }
-      ++gd;
-      if (++db == 2) {
-        db = 0;
-        dph ^= 1;
+        if (seg_end) {
+          ++gd;
+          if (++db == 2) {
+            db = 0;
+            dph ^= 1;
+          }
+        }
       }
     }
   } else if (warp >= 4) {
@@ -261,32 +268,44 @@ __global__ void __launch_bounds__(THREADS, 1) igemm_kernel(const __grid_constant
         ok = h >= 0 && h < p.H && w >= 0 && w < p.W;
       }
       const size_t pix = (size_t)n * p.Cout * plane + (size_t)h * p.W + w;
-      mbar_wait(&d_full[db], dph);
-      tc_fence_after();
-      const uint32_t a = tmem + ((uint32_t)(qd * 32) << 16) + db * p.NN + eh * half;
-      for (int c0 = 0; c0 < half; c0 += 16) {
-        float v[16];
-        tmem_ld16(a + c0, v);
-        tmem_wait_ld();
-        if (ok) {
+      const int nseg = (p.NC + p.seg - 1) / p.seg;
+      for (int sg = 0; sg < nseg; ++sg) {
+        // long reductions (Cin > 8*64) are cut into segments of <= 4608 K: each segment is a
+        // fresh TMEM accumulation, added here in FP32 (same thread, program order); the
+        // tensor-core accumulation error grows with the K of one accumulator
+        // (profiles/r01/igemm/acc_probe.txt), the sum of segments only with its square root
+        const bool first = sg == 0, last = sg == nseg - 1;
+        mbar_wait(&d_full[db], dph);
+        tc_fence_after();
+        const uint32_t a = tmem + ((uint32_t)(qd * 32) << 16) + db * p.NN + eh * half;
+        for (int c0 = 0; c0 < half; c0 += 16) {
+          float v[16];
+          tmem_ld16(a + c0, v);
+          tmem_wait_ld();
+          if (ok) {
 #pragma unroll
-          for (int j = 0; j < 16; ++j) {
-            const int co = ct * p.NN + eh * half + c0 + j;
-            if (co < p.Cout) {
-              float r = v[j] + (p.bias ? p.bias[co] : 0.f);
-              if (p.act == RC_ACT_RELU) r = fmaxf(r, 0.f);
-              p.y[pix + (size_t)co * plane] = r;
-              if (p.am) p.am[pix + (size_t)co * plane] = 0;
+            for (int j = 0; j < 16; ++j) {
+              const int co = ct * p.NN + eh * half + c0 + j;
+              if (co < p.Cout) {
+                float* yp = p.y + pix + (size_t)co * plane;
+                float r = first ? v[j] : *yp + v[j];
+                if (last) {
+                  r += p.bias ? p.bias[co] : 0.f;
+                  if (p.act == RC_ACT_RELU) r = fmaxf(r, 0.f);
+                  if (p.am) p.am[pix + (size_t)co * plane] = 0;
+                }
+                *yp = r;
+              }
             }
           }
         }
-      }
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&d_empty[db]);
-      if (++db == 2) {
-        db = 0;
-        dph ^= 1;
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&d_empty[db]);
+        if (++db == 2) {
+          db = 0;
+          dph ^= 1;
+        }
       }
     }
   }
@@ -411,6 +430,11 @@ int launch_igemm(const rc_desc& d, const float* x, const uint8_t* wpk, const uin
   p.x_stages = plan.x_stages;
   p.w_stages = plan.w_stages;
   p.act = d.activation;
+  {
+    const char* se = getenv("RC_IGEMM_SEG");  // A/B: chunks per accumulation segment
+    p.seg = se ? atoi(se) : 8;
+    if (p.seg < 1) p.seg = 1;
+  }
   TapOffsets to;
   slice_tap_offsets(3, d.convention, &to);
   for (int t = 0; t < 9; ++t) p.off[t] = to.di[0][t] * g.Wp + to.dj[0][t];
