@@ -105,7 +105,8 @@ def test_backward_vs_float64_autograd(dev, case, precision, tol):
 
 
 @pytest.mark.parametrize("case", [(2, 256, 16, 16, 1024, "steer", 8, "subgroup", 4, "scatter", "none"),
-                                  (3, 64, 32, 32, 128, "p4m", 8, "max", 8, "scatter", "relu")],
+                                  (3, 64, 32, 32, 128, "p4m", 8, "max", 8, "scatter", "relu"),
+                                  (256, 32, 16, 16, 32, "p4", 4, "avg", 4, "scatter", "none")],
                          ids=lambda c: "-".join(map(str, c)))
 def test_backward_large_tensor_core(dev, case):
     """The C3 layer shape (tensor-core weight gradient without K splits: 512 work items) and a
