@@ -344,7 +344,14 @@ int rc_ri_conv_backward(const rc_desc* d, const float* d_x, const void* d_bank, 
                         const uint8_t* d_argmax, float* d_dx, float* d_dw0, float* d_dw1, float* d_dbias,
                         float* d_scratch, void* d_ws, size_t ws_bytes, void* stream) {
   RC_CHECK_DESC(d);
-  if (d->n == 0) return RC_OK;
+  if (d->n == 0) {  // empty batch: zero parameter gradients (dx is empty)
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const size_t wb = (size_t)d->c_out * d->c_in * d->k * d->k * sizeof(float);
+    if (d_dw0) RC_CUDA(cudaMemsetAsync(d_dw0, 0, wb, s));
+    if (d_dw1 && d->group == RC_GROUP_STEER) RC_CUDA(cudaMemsetAsync(d_dw1, 0, wb, s));
+    if (d_dbias) RC_CUDA(cudaMemsetAsync(d_dbias, 0, (size_t)d->c_out * sizeof(float), s));
+    return RC_OK;
+  }
   if (!d_gy || !d_bank || !d_scratch) return fail(RC_ERR_INVALID, "ri_conv_backward: null pointer");
   if ((d->pool == RC_POOL_MAX || d->pool == RC_POOL_SUBGROUP) && !d_argmax)
     return fail(RC_ERR_INVALID, "pool_backward_max: argmax map required");

@@ -42,7 +42,7 @@ struct WgParams {
   const uint8_t* xl;  // lo plane or null
   float* out;         // dF, or the split partials [split][M][Ncol]
   long long xrows_plane;
-  int M, MT, Cin, NCc, KC, splits, items, parts, passes, stages, xr, G, Wp;
+  int M, MT, Cin, NCc, KC, splits, per, items, parts, passes, stages, xr, G, Wp;
   int off[9];         // row offset of gather position pos
 };
 
@@ -121,9 +121,8 @@ __device__ __forceinline__ Item decode(const WgParams& p, int item) {
   r /= 2;
   it.cc = r % p.NCc;
   it.mt = r / p.NCc;
-  const int per = (p.KC + p.splits - 1) / p.splits;
-  it.k0 = it.split * per;
-  it.k1 = min(p.KC, it.k0 + per);
+  it.k0 = it.split * p.per;  // host: splits = ceil(KC / per), so no split is empty
+  it.k1 = min(p.KC, it.k0 + p.per);
   it.t0 = it.tg ? 5 : 0;
   it.nt = it.tg ? 4 : 5;
   return it;
@@ -248,7 +247,7 @@ __global__ void __launch_bounds__(THREADS, 1) wgrad_kernel(const __grid_constant
 }
 
 struct WgGeom {
-  int M, MT, NCc, KC, xr, parts, splits, stages;
+  int M, MT, NCc, KC, xr, parts, splits, per, stages;
   long long QN;
   size_t gp_bytes, x_bytes, part_bytes, smem;
 };
@@ -265,7 +264,9 @@ WgGeom wg_geom(const rc_desc& d) {
   const int base = g.MT * g.NCc * 2;
   int sp = (296 + base - 1) / base;
   const int maxsp = g.KC / 16 > 1 ? g.KC / 16 : 1;
-  g.splits = sp < 1 ? 1 : (sp > maxsp ? maxsp : sp);
+  sp = sp < 1 ? 1 : (sp > maxsp ? maxsp : sp);
+  g.per = g.KC > 0 ? (g.KC + sp - 1) / sp : 1;
+  g.splits = g.KC > 0 ? (g.KC + g.per - 1) / g.per : 1;
   const size_t stage = (size_t)g.parts * (ATILE + (size_t)g.xr * 128);
   const size_t cap = 232448 - 1024 - 512;
   g.stages = (int)(cap / stage) > MAX_STAGES ? MAX_STAGES : (int)(cap / stage);
@@ -319,6 +320,7 @@ int launch_wgrad(const rc_desc& d, const float* x, const float* df, float* dF, v
   p.NCc = g.NCc;
   p.KC = g.KC;
   p.splits = g.splits;
+  p.per = g.per;
   p.items = g.MT * g.NCc * 2 * g.splits;
   p.parts = g.parts;
   p.passes = g.parts == 2 ? 3 : 1;

@@ -141,6 +141,38 @@ def test_backward_large_tensor_core(dev, case):
     assert errs["db"] <= 1e-5, errs
 
 
+def test_weight_gradient_many_k_splits(dev):
+    """A thin layer over a large batch: 1 m-tile x 1 ci-chunk, so the tensor-core weight
+    gradient splits K over ~143 work items (no split may be empty) and reduces them."""
+    import paper_2512_08888_b200 as P
+    n, cin, h, w, cout = 480, 8, 16, 16, 16
+    desc = P.Desc(n, cin, h, w, cout, 3, "p4", 4, "avg", 4, "scatter", "bf16x3")
+    gen = torch.Generator(device=dev).manual_seed(23)
+    x = torch.rand((n, cin, h, w), generator=gen, device=dev) * 2 - 1
+    w0 = (torch.rand((cout, cin, 3, 3), generator=gen, device=dev) * 2 - 1) / math.sqrt(cin * 9)
+    bank = P.bank_precompute(desc, w0)
+    y, am = P.ri_conv_forward(desc, x, bank)
+    m = torch.rand(y.shape, generator=gen, device=dev) * 2 - 1
+    _, dw0, _, _ = P.ri_conv_backward(desc, x, bank, m, y, am, need_input=False, need_bias=False)
+    w0d = w0.double().requires_grad_()
+    (ref_forward(x.double(), w0d, None, None, desc, am) * m.double()).sum().backward()
+    err = ((dw0.double() - w0d.grad).abs().max() / w0d.grad.abs().max()).item()
+    assert err <= 1e-4, err
+
+
+def test_empty_batch_zero_parameter_gradients(dev):
+    import paper_2512_08888_b200 as P
+    desc = P.Desc(0, 16, 8, 8, 32, 3, "steer", 8, "subgroup", 4, "scatter", "auto")
+    x = torch.empty((0, 16, 8, 8), device=dev)
+    w0 = torch.rand((32, 16, 3, 3), device=dev)
+    w1 = torch.rand((32, 16, 3, 3), device=dev)
+    bank = P.bank_precompute(desc, w0, w1)
+    gy = torch.empty((0, 32, 2, 8, 8), device=dev)
+    am = torch.empty(gy.shape, dtype=torch.uint8, device=dev)
+    _, dw0, dw1, db = P.ri_conv_backward(desc, x, bank, gy, None, am)
+    assert not dw0.any() and not dw1.any() and not db.any()
+
+
 def test_autograd_function_and_zero_upstream(dev):
     import paper_2512_08888_b200 as P
     desc = P.Desc(2, 16, 16, 16, 32, 3, "steer", 8, "subgroup", 4, "scatter", "auto", "relu")
