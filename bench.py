@@ -219,6 +219,44 @@ def run_reference(args, wl):
     print(json.dumps(out), flush=True)
 
 
+def smem_traffic(desc, kernel: str):
+    """Shared-memory bytes one launch of the band kernel (ri_tc.cu) moves, from its geometry:
+    per K-step (16 ci of one chunk) the SS MMAs read A = passes_A x 4 KB of weights and
+    B = passes_B x N x 32 B of the X band (bf16x3: Ah twice + Al once, Xh twice + Xl once),
+    and the TMA writes parts x 4 KB of weights; plus the X band writes.  None for other kernels."""
+    if not (kernel.startswith("tc_k3w16") or kernel.startswith("tc_k3strip")):
+        return None
+    three = kernel.endswith("bf16x3")
+    parts, pa = (2, 3) if three else (1, 1)
+    n, h, w, cin, cout = desc.n, desc.h, desc.w, desc.c_in, desc.c_out
+    NB = {"single": 1, "p4": 1, "p4m": 2, "steer": desc.orientations // 4}[desc.group]
+    NC = (cin + 63) // 64
+    NCT = (cout + 127) // 128
+    if kernel.startswith("tc_k3w16"):  # bands of 4 rows; full-row bands skip out-of-image halo rows
+        bands = []
+        for k in range((h + 3) // 4):
+            r0 = 4 * k - 1
+            lo, hi = (1 if r0 < 0 else 0), min(6, h - r0)
+            bands.append((hi - lo) * 16)
+    else:  # 4x16 strips of 6x18 input px, N = 112
+        bands = [112] * (((h + 3) // 4) * (w // 16))
+    kstep = lambda N: pa * 4096 + pa * N * 32 + parts * 4096
+    per_item = sum(NB * 9 * NC * 4 * kstep(N) + parts * NC * N * 128 for N in bands)
+    return per_item * n * NCT
+
+
+def smem_roofline(desc, kernel_ms):
+    """The band kernel's binding roofline: shared-memory bandwidth (SS operand reads + TMA
+    writes), 128 B/cycle/SM x 148 SMs at the max SM clock (37.2 TB/s)."""
+    b = smem_traffic(desc, desc.kernel_name())
+    if b is None or not kernel_ms:
+        return None
+    ach = b / (kernel_ms * 1e-3) / 1e12
+    peak = 128 * 148 * 1.965e9 / 1e12
+    return {"bytes_per_launch": b, "achieved": ach, "peak": peak, "unit": "TB/s", "frac": ach / peak,
+            "note": "SS MMA operand reads + TMA weight/X writes per launch (bench.smem_traffic), / main-kernel time"}
+
+
 def backward_context(P, desc, x, bank, y, am, reps=3):
     """The layer's backward (SPEC backward module: pool/ReLU/bias backward, input gradient,
     weight gradient) on the same inputs, CUDA-event timed after one warm-up; context for the
@@ -591,6 +629,7 @@ def main():
                                          "derived FP32 FFMA peak 148 SM x 128 x 2 x 1.965 GHz"),
                          "mma_passes": passes,
                          "frac_of_pass_ceiling": achieved * passes / tpeak if tc else None,
+                         "smem": smem_roofline(desc, kernel_ms),
                          "note": "achieved = algorithmic FLOPs 2*N*H*W*K^2*Cin*Cout*B per launch / the main "
                                  "kernel's CUDA-event time (rc_profile_*; operand packing excluded). bf16x3 "
                                  "issues 3 bf16 MMAs per FP32-class product: frac_of_pass_ceiling = "
