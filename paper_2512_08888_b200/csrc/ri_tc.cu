@@ -48,6 +48,16 @@ using namespace tc;
 //   TW = 8, 4 (H == W): small images, whole images per band and no halo rows at all (the
 //             window rows outside an image are the zero padding): 1 image of 8x8 or 4
 //             images of 4x4 per band (N = 64); a thread owns TR = 16/W full rows.
+// Experiment (off): bf16x3 with the hi weight tile (read by 2 of the 3 products) copied to
+// TMEM once per chunk with tcgen05.cp and consumed by TS MMAs, so shared memory serves Ah
+// once instead of twice.  Bit-identical, but 15% slower on C3 and C4
+// (profiles/r01/tsa_ab.txt): the copy -> MMA dependency costs more than the saved reads.
+#ifndef RC_TC_TSA
+#define RC_TC_TSA 0
+#endif
+constexpr bool kTsa = RC_TC_TSA != 0;
+constexpr uint32_t A_COL0 = 448;  // TMEM columns [448, 512): two Ah regions
+
 template <int TW>
 struct Geo {
   static constexpr bool STRIP = TW == 0;
@@ -63,7 +73,9 @@ struct Geo {
   // first pixel inside the allocation; full-row bands also read their skipped (out-of-image)
   // window rows from them as zeros (band_rows), so they need D0 >= 18.
   static constexpr uint32_t D0 = (STRIP || SMALL) ? 16 : 32;
-  static constexpr int NDB = MMA_N * 5 + D0 <= 512 ? 5 : (MMA_N * 4 + D0 <= 512 ? 4 : 3);  // TMEM D buffers
+  // bf16x3 with Ah staged in TMEM (kTsa) keeps 2 x 32 columns at the top for it
+  static constexpr uint32_t TOP = kTsa ? 64 : 0;
+  static constexpr int NDB = MMA_N * 5 + D0 + TOP <= 512 ? 5 : (MMA_N * 4 + D0 + TOP <= 512 ? 4 : 3);  // D buffers
   static constexpr int TR = SMALL ? 16 / TW : 1;              // output rows per epilogue thread
   static constexpr int IMGS = SMALL ? 64 / (TW * TW) : 1;     // images per band
 };
@@ -681,7 +693,7 @@ __global__ void __launch_bounds__(THREADS, 1) ri_tc_kernel(const __grid_constant
     const uint32_t idesc = idesc_bf16_f32(PAIR ? 256 : 128, G::MMA_N);
     const uint32_t xaddr = smem_u32(xs);
     Ring wr;
-    uint32_t xc = 0, gd = 0;
+    uint32_t xc = 0, gd = 0, areg = 0;
     int db = 0;
     uint32_t dph = 0;
     for (int item = wk.first; item < wk.count; item += wk.stride) {
@@ -724,6 +736,19 @@ __global__ void __launch_bounds__(THREADS, 1) ri_tc_kernel(const __grid_constant
                   const uint32_t xl_a = p.xstream ? wbase + stage_w + (p.spc + cl) * XS : xaddr + (p.NC + c) * XS;
                   const uint64_t bh = desc_k_sw128(xh_a + xoff_k);
                   const uint64_t ah = desc_k_sw128(wbase + cl * parts * WTILE);
+                  if (kTsa && !PAIR && parts == 2) {
+                    const uint32_t atm = tmem + A_COL0 + (areg++ & 1) * 32;
+#pragma unroll
+                    for (int kk = 0; kk < 4; ++kk) tmem_cp_128x256b(atm + 8 * kk, ah + 2 * kk);
+#pragma unroll
+                    for (int kk = 0; kk < 4; ++kk) mma_bf16_ts(d, atm + 8 * kk, bh + 2 * kk, idesc_k, (c | kk) != 0);
+                    const uint64_t bl = desc_k_sw128(xl_a + xoff_k);
+                    const uint64_t al = desc_k_sw128(wbase + (cl * parts + 1) * WTILE);
+#pragma unroll
+                    for (int kk = 0; kk < 4; ++kk) mma_bf16_ts(d, atm + 8 * kk, bl + 2 * kk, idesc_k, 1);
+#pragma unroll
+                    for (int kk = 0; kk < 4; ++kk) mma_bf16_ss(d, al + 2 * kk, bh + 2 * kk, idesc_k, 1);
+                  } else {
 #pragma unroll
                   for (int kk = 0; kk < 4; ++kk) {
                     if constexpr (PAIR)
@@ -748,6 +773,7 @@ __global__ void __launch_bounds__(THREADS, 1) ri_tc_kernel(const __grid_constant
                       else
                         mma_bf16_ss(d, al + 2 * kk, bh + 2 * kk, idesc_k, 1);
                     }
+                  }
                   }
                   if (t == 8 && b == p.NB - 1 && !p.xstream) {  // chunk c of this band fully consumed
                     if constexpr (PAIR)
