@@ -365,8 +365,11 @@ struct SimtK3 {
   }
 };
 
+#ifndef RC_SIMT_MINB
+#define RC_SIMT_MINB 1  // resident CTAs per SM the register allocation targets (A/B builds)
+#endif
 template <int SW, int S, int RPB, int CONV>
-__global__ void __launch_bounds__(256, 1) simt_k3_kernel(Params p) {
+__global__ void __launch_bounds__(256, RC_SIMT_MINB) simt_k3_kernel(Params p) {
   extern __shared__ __align__(16) float smem[];
   SimtK3<SW, S, RPB, CONV> k(p, smem);
   k.run();
