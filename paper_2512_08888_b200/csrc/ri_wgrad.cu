@@ -43,6 +43,8 @@ struct WgParams {
   float* out;         // dF, or the split partials [split][M][Ncol]
   long long xrows_plane;
   int M, MT, Cin, NCc, KC, splits, per, items, parts, passes, stages, xr, G, Wp;
+  int nci;            // X planes (64 ci each) per work item: 2 -> N = 128 (MN atoms LBO apart)
+  int tgs, ntg;       // taps per group, tap groups (N=64: 5 + 4, N=128: 3 + 3 + 3)
   int off[9];         // row offset of gather position pos
 };
 
@@ -117,14 +119,14 @@ __device__ __forceinline__ Item decode(const WgParams& p, int item) {
   Item it;
   it.split = item % p.splits;
   int r = item / p.splits;
-  it.tg = r % 2;
-  r /= 2;
+  it.tg = r % p.ntg;
+  r /= p.ntg;
   it.cc = r % p.NCc;
   it.mt = r / p.NCc;
   it.k0 = it.split * p.per;  // host: splits = ceil(KC / per), so no split is empty
   it.k1 = min(p.KC, it.k0 + p.per);
-  it.t0 = it.tg ? 5 : 0;
-  it.nt = it.tg ? 4 : 5;
+  it.t0 = it.tg * p.tgs;
+  it.nt = min(p.tgs, 9 - it.t0);
   return it;
 }
 
@@ -134,8 +136,9 @@ __global__ void __launch_bounds__(THREADS, 1) wgrad_kernel(const __grid_constant
   __shared__ __align__(8) uint64_t full[MAX_STAGES], empty[MAX_STAGES], d_full, d_empty;
   __shared__ uint32_t tmem_base;
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-  const uint32_t XB = (uint32_t)p.xr * 128;            // bytes of one X part per stage
-  const uint32_t stage = p.parts * (ATILE + XB);
+  const uint32_t XB = (uint32_t)p.xr * 128;            // bytes of one X plane block per stage
+  const uint32_t XP = p.nci * XB;                      // one part (hi or lo): nci plane blocks
+  const uint32_t stage = p.parts * (ATILE + XP);
   if (threadIdx.x == 0) {
     for (int i = 0; i < MAX_STAGES; ++i) {
       mbar_init(&full[i], 1);
@@ -163,9 +166,11 @@ __global__ void __launch_bounds__(THREADS, 1) wgrad_kernel(const __grid_constant
           mbar_arrive_expect_tx(&full[r.s], stage);
           bulk_g2s(dst, p.gp + ((size_t)it.mt * p.KC + kc) * p.parts * ATILE, p.parts * ATILE, &full[r.s]);
           const long long r0 = ((long long)p.G + (long long)kc * KQ - p.Wp - 1) & ~7LL;
-          const size_t src = ((size_t)it.cc * p.xrows_plane + r0) * 128;
-          bulk_g2s(dst + p.parts * ATILE, p.xh + src, XB, &full[r.s]);
-          if (p.parts == 2) bulk_g2s(dst + p.parts * ATILE + XB, p.xl + src, XB, &full[r.s]);
+          for (int pl = 0; pl < p.nci; ++pl) {
+            const size_t src = ((size_t)(it.cc * p.nci + pl) * p.xrows_plane + r0) * 128;
+            bulk_g2s(dst + p.parts * ATILE + pl * XB, p.xh + src, XB, &full[r.s]);
+            if (p.parts == 2) bulk_g2s(dst + p.parts * ATILE + XP + pl * XB, p.xl + src, XB, &full[r.s]);
+          }
         }
         __syncwarp();
         r.adv(p.stages);
@@ -173,7 +178,11 @@ __global__ void __launch_bounds__(THREADS, 1) wgrad_kernel(const __grid_constant
     }
   } else if (warp == 1) {
     // ---------------------------------------------------------------- MMA issuer
-    const uint32_t idesc = idesc_bf16_f32(128, 64) | (1u << 16);  // B (X rows) MN-major
+    const uint32_t NT = 64 * p.nci;
+    const uint32_t idesc = idesc_bf16_f32(128, NT) | (1u << 16);  // B (X rows) MN-major
+    // MN-major B: the second 64-ci atom lies XB bytes after the first (leading-byte offset)
+    const uint64_t lbo = (uint64_t)(((p.nci == 2 ? XB : 16) >> 4) & 0x3FFF) << 16;
+    auto bdesc = [&](uint32_t a) { return (desc_k_sw128(a) & ~(0x3FFFull << 16)) | lbo; };
     Ring r;
     int n_items = 0;
     for (int item = blockIdx.x; item < p.items; item += gridDim.x, ++n_items) {
@@ -190,9 +199,9 @@ __global__ void __launch_bounds__(THREADS, 1) wgrad_kernel(const __grid_constant
           const uint32_t row0 = (uint32_t)(p.G + (long long)kc * KQ - r0);
           const uint32_t xb = base + p.parts * ATILE;
           for (int tt = 0; tt < it.nt; ++tt) {
-            const uint32_t d = tmem + tt * 64;
+            const uint32_t d = tmem + tt * NT;
             const uint32_t xrow = (row0 + p.off[it.t0 + tt]) * 128;
-            const uint64_t xh = desc_k_sw128(xb + xrow), xl = desc_k_sw128(xb + XB + xrow);
+            const uint64_t xh = bdesc(xb + xrow), xl = bdesc(xb + XP + xrow);
             const uint32_t acc0 = kc != it.k0;
 #pragma unroll
             for (int kk = 0; kk < 4; ++kk) mma_bf16_ss(d, gh + 2 * kk, xh + (uint64_t)(kk * 128), idesc, acc0 | kk);
@@ -221,16 +230,17 @@ __global__ void __launch_bounds__(THREADS, 1) wgrad_kernel(const __grid_constant
       tc_fence_after();
       const int m = it.mt * 128 + qd * 32 + lane;
       float* dst = p.out + (size_t)it.split * p.M * Ncol + (size_t)m * Ncol;
+      const int NT = 64 * p.nci;
       for (int tt = 0; tt < it.nt; ++tt) {
         const int pos = it.t0 + tt;
-        for (int c0 = 0; c0 < 64; c0 += 16) {
+        for (int c0 = 0; c0 < NT; c0 += 16) {
           float v[16];
-          tmem_ld16(tmem + ((uint32_t)(qd * 32) << 16) + tt * 64 + c0, v);
+          tmem_ld16(tmem + ((uint32_t)(qd * 32) << 16) + tt * NT + c0, v);
           tmem_wait_ld();
           if (m < p.M) {
 #pragma unroll
             for (int j = 0; j < 16; ++j) {
-              const int ci = it.cc * 64 + c0 + j;
+              const int ci = it.cc * NT + c0 + j;
               if (ci < p.Cin) dst[(size_t)ci * 9 + pos] = v[j];
             }
           }
@@ -247,7 +257,7 @@ __global__ void __launch_bounds__(THREADS, 1) wgrad_kernel(const __grid_constant
 }
 
 struct WgGeom {
-  int M, MT, NCc, KC, xr, parts, splits, per, stages;
+  int M, MT, NCc, KC, xr, parts, splits, per, stages, nci, tgs, ntg;
   long long QN;
   size_t gp_bytes, x_bytes, part_bytes, smem;
 };
@@ -256,18 +266,28 @@ WgGeom wg_geom(const rc_desc& d) {
   const PadGeom pg = pad_geom(d);
   g.M = d.c_out * num_bases(d) * rot_per_base(d);
   g.MT = (g.M + 127) / 128;
-  g.NCc = pg.NC;
+  // 128-ci tiles (N = 128: math-bound MMAs, 3 taps x 128 TMEM columns) when the planes pair
+  // up, else 64-ci tiles (N = 64: shared-memory bound, 5 + 4 taps); RC_WGRAD_N=64 forces 64
+  const char* en = getenv("RC_WGRAD_N");
+  g.nci = (pg.NC % 2 == 0 && !(en && atoi(en) == 64)) ? 2 : 1;
+  g.parts = d.precision == RC_PREC_BF16 ? 1 : 2;
+  g.xr = (KQ + 2 * (pg.Wp + 1) + 7 + 7) / 8 * 8;
+  const size_t cap0 = 232448 - 1024 - 512;
+  if (g.nci == 2 && cap0 / ((size_t)g.parts * (ATILE + 2 * (size_t)g.xr * 128)) < 2) g.nci = 1;  // wide images
+  g.tgs = g.nci == 2 ? 3 : 5;
+  g.ntg = (9 + g.tgs - 1) / g.tgs;
+  g.NCc = pg.NC / g.nci;
   g.QN = (long long)d.n * pg.Pimg;
   g.KC = (int)((g.QN + KQ - 1) / KQ);
   g.xr = (KQ + 2 * (pg.Wp + 1) + 7 + 7) / 8 * 8;
   g.parts = d.precision == RC_PREC_BF16 ? 1 : 2;
-  const int base = g.MT * g.NCc * 2;
+  const int base = g.MT * g.NCc * g.ntg;
   int sp = (296 + base - 1) / base;
   const int maxsp = g.KC / 16 > 1 ? g.KC / 16 : 1;
   sp = sp < 1 ? 1 : (sp > maxsp ? maxsp : sp);
   g.per = g.KC > 0 ? (g.KC + sp - 1) / sp : 1;
   g.splits = g.KC > 0 ? (g.KC + g.per - 1) / g.per : 1;
-  const size_t stage = (size_t)g.parts * (ATILE + (size_t)g.xr * 128);
+  const size_t stage = (size_t)g.parts * (ATILE + (size_t)g.nci * g.xr * 128);
   const size_t cap = 232448 - 1024 - 512;
   g.stages = (int)(cap / stage) > MAX_STAGES ? MAX_STAGES : (int)(cap / stage);
   g.smem = (size_t)g.stages * stage + 1024;
@@ -321,7 +341,10 @@ int launch_wgrad(const rc_desc& d, const float* x, const float* df, float* dF, v
   p.KC = g.KC;
   p.splits = g.splits;
   p.per = g.per;
-  p.items = g.MT * g.NCc * 2 * g.splits;
+  p.nci = g.nci;
+  p.tgs = g.tgs;
+  p.ntg = g.ntg;
+  p.items = g.MT * g.NCc * g.ntg * g.splits;
   p.parts = g.parts;
   p.passes = g.parts == 2 ? 3 : 1;
   p.stages = g.stages;

@@ -18,10 +18,12 @@ timeout -s KILL 900 python bench.py --impl reference --steps 3 --warmup 1 > $O/b
 timeout -s KILL 1500 python tools/appendix_sweep.py --out $O/c2 > $O/c2/sweep.log 2>&1; echo rc=$? >> $O/c2/sweep.log
 timeout -s KILL 1500 python tools/bench_cli.py --sizes 8 16 32 --cin 64 256 --cout 256 1024 --orientations 8 --group steer --batch 32 --out $O/bench_cli_r8.md --format md > $O/bench_cli_r8.log 2>&1; echo rc=$? >> $O/bench_cli_r8.log
 NCU=/usr/local/cuda/bin/ncu
-for w in c3 c4 c1 c5; do
+for w in c3 c4 c1; do
 timeout -s KILL 600 $NCU --metrics gpu__time_duration.sum --clock-control none -c 60 --csv --log-file $O/launches_$w.csv \
   python bench.py --workload $w --steps 2 --warmup 3 --no-cpu-baseline --e2e-steps 1 > $O/ncu_launch_$w.log 2>&1
 done
+timeout -s KILL 600 $NCU --metrics gpu__time_duration.sum --clock-control none -k regex:"simt_k3|igemm|ig_pack|x_pack|ri_tc|maxpool|gap_linear" -c 40 --csv \
+  --log-file $O/launches_c5.csv python bench.py --workload c5 --steps 1 --warmup 3 --no-cpu-baseline --e2e-steps 1 > $O/ncu_launch_c5.log 2>&1
 timeout -s KILL 900 $NCU --set full --clock-control none --import-source on -k regex:ri_tc_kernel -s 3 -c 1 -o $O/tc_c3 \
   python bench.py --steps 1 --warmup 3 --no-cpu-baseline --e2e-steps 1 > $O/ncu_full_c3.log 2>&1
 timeout -s KILL 900 $NCU --set full --clock-control none --import-source on -k regex:ri_tc_kernel -s 3 -c 1 -o $O/tc_c4 \

@@ -100,6 +100,52 @@ __global__ void __launch_bounds__(128, 1)
   if (warp == 0) tmem_dealloc<512>(tbase);
 }
 
+// MN-major B with N = 128: two 64-wide MN atoms [BR k][64 n] stored `lbo` bytes apart (the
+// descriptor's leading-byte offset), row shift s as before.
+__global__ void __launch_bounds__(128, 1)
+    probe_mn128(int s, int lbo, const __nv_bfloat16* Ag, const __nv_bfloat16* Bg, float* out) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  __nv_bfloat16* sA = reinterpret_cast<__nv_bfloat16*>(smem);
+  uint8_t* sB = smem + 128 * 128;
+  __shared__ uint64_t bar;
+  __shared__ uint32_t tbase;
+  const int tid = threadIdx.x, warp = tid / 32;
+  for (int i = tid; i < 128 * 64; i += blockDim.x) sA[sw128_offset(i / 64, i % 64) / 2] = Ag[i];
+  for (int i = tid; i < BR * 128; i += blockDim.x) {  // Bg [k][128 n]
+    const int k = i / 128, n = i % 128;
+    reinterpret_cast<__nv_bfloat16*>(sB + (n / 64) * lbo)[sw128_offset(k, n % 64) / 2] = Bg[i];
+  }
+  fence_proxy_async_smem();
+  if (warp == 0) tmem_alloc<512>(&tbase);
+  if (tid == 0) {
+    mbar_init(&bar, 1);
+    fence_barrier_init();
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (tid == 0) {
+    const uint64_t da = desc_k_sw128(smem_u32(sA));
+    uint64_t db = desc_k_sw128(smem_u32(sB) + 128 * s);
+    db = (db & ~(0x3FFFull << 16)) | ((uint64_t)((lbo >> 4) & 0x3FFF) << 16);
+    const uint32_t idesc = idesc_bf16_f32(128, 128) | (1u << 16);
+    for (int kk = 0; kk < 4; ++kk) mma_bf16_ss(tbase, da + 2 * kk, db + (uint64_t)(kk * 2048 >> 4), idesc, kk != 0);
+    mma_commit(&bar);
+  }
+  mbar_wait(&bar, 0);
+  tc_fence_after();
+  float v[32];
+  for (int c = 0; c < 128; c += 32) {
+    tmem_ld32(tbase + ((uint32_t)(warp * 32) << 16) + c, v);
+    tmem_wait_ld();
+    for (int j = 0; j < 32; ++j) out[tid * 128 + c + j] = v[j];
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) tmem_dealloc<512>(tbase);
+}
+
 int main() {
   std::vector<__nv_bfloat16> A(AR * 64), B(N * 64);
   std::vector<float> Af(AR * 64), Bf(N * 64);
@@ -165,6 +211,40 @@ int main() {
           if (ref != o2[m * 64 + n]) ++bad;
         }
       printf("{\"mn_shift\":%d,\"mismatches\":%d}\n", s, bad);
+    }
+  }
+  {  // MN-major B, N = 128 (two atoms LBO apart)
+    std::vector<__nv_bfloat16> A3(128 * 64), B3(BR * 128);
+    std::vector<float> A3f(128 * 64), B3f(BR * 128);
+    for (int i = 0; i < 128 * 64; ++i) A3[i] = __float2bfloat16(A3f[i] = (float)(rand() % 9 - 4));
+    for (int i = 0; i < BR * 128; ++i) B3[i] = __float2bfloat16(B3f[i] = (float)(rand() % 9 - 4));
+    __nv_bfloat16 *dA3, *dB3;
+    float* dout3;
+    cudaMalloc(&dA3, A3.size() * 2);
+    cudaMalloc(&dB3, B3.size() * 2);
+    cudaMalloc(&dout3, 128 * 128 * 4);
+    cudaMemcpy(dA3, A3.data(), A3.size() * 2, cudaMemcpyHostToDevice);
+    cudaMemcpy(dB3, B3.data(), B3.size() * 2, cudaMemcpyHostToDevice);
+    const int lbo = BR * 128;  // second atom right after the first [BR x 128 B] block
+    const int sm3 = 128 * 128 + 2 * lbo + 2048;
+    cudaFuncSetAttribute(probe_mn128, cudaFuncAttributeMaxDynamicSharedMemorySize, sm3);
+    std::vector<float> o3(128 * 128);
+    for (int s : {0, 1, 5, 9, 37}) {
+      probe_mn128<<<1, 128, sm3>>>(s, lbo, dA3, dB3, dout3);
+      cudaError_t e = cudaDeviceSynchronize();
+      if (e != cudaSuccess) {
+        printf("{\"mn128_shift\":%d,\"error\":\"%s\"}\n", s, cudaGetErrorString(e));
+        return 1;
+      }
+      cudaMemcpy(o3.data(), dout3, o3.size() * 4, cudaMemcpyDeviceToHost);
+      int bad = 0;
+      for (int m = 0; m < 128; ++m)
+        for (int n = 0; n < 128; ++n) {
+          float ref = 0;
+          for (int k = 0; k < 64; ++k) ref += A3f[m * 64 + k] * B3f[(s + k) * 128 + n];
+          if (ref != o3[m * 128 + n]) ++bad;
+        }
+      printf("{\"mn128_shift\":%d,\"lbo\":%d,\"mismatches\":%d}\n", s, lbo, bad);
     }
   }
   return 0;
