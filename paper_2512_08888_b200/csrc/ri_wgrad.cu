@@ -70,13 +70,13 @@ __global__ void __launch_bounds__(256) g_pack_kernel(const float* __restrict__ g
     long long q = kc * KQ + grp * 8;
     int n = (int)(q / Pimg), rem = (int)(q - (long long)n * Pimg);
     int hp = rem / Wp, wp = rem - hp * Wp;
-    __align__(16) __nv_bfloat16 h8[8], l8[8];
+    // addresses first (the pixel walk is sequential), then 8 independent loads in flight
+    long long src[8];
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
-      float v = 0.f;
-      if (m < M && q + j < QN && hp >= 1 && hp <= H && wp >= 1 && wp <= W)
-        v = g[((size_t)n * M + m) * plane + (size_t)(hp - 1) * W + (wp - 1)];
-      split_bf16(v, h8[j], l8[j]);
+      src[j] = (m < M && q + j < QN && hp >= 1 && hp <= H && wp >= 1 && wp <= W)
+                   ? ((long long)n * M + m) * (long long)plane + (long long)(hp - 1) * W + (wp - 1)
+                   : -1;
       if (++wp == Wp) {
         wp = 0;
         if (++hp == H + 2) {
@@ -85,6 +85,12 @@ __global__ void __launch_bounds__(256) g_pack_kernel(const float* __restrict__ g
         }
       }
     }
+    float v[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) v[j] = src[j] >= 0 ? __ldg(g + src[j]) : 0.f;
+    __align__(16) __nv_bfloat16 h8[8], l8[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) split_bf16(v[j], h8[j], l8[j]);
     const size_t tile = ((size_t)mt * KC + kc) * parts;
     const size_t off = (size_t)ml * 128 + (size_t)((grp ^ (ml & 7)) << 4);
     *reinterpret_cast<uint4*>(gp + tile * ATILE + off) = *reinterpret_cast<const uint4*>(h8);
