@@ -25,6 +25,10 @@
 #include "k3_tables.cuh"
 #include "rc_internal.cuh"
 
+#ifndef RC_SIMT_ROT
+#define RC_SIMT_ROT 1  // 1: one step body + register ring rotation; 0: three unrolled ring phases
+#endif
+
 namespace rc {
 namespace {
 
@@ -355,11 +359,26 @@ struct SimtK3 {
     else
       issue(0, total);
     for (int b = 0; b < p.NB; ++b) {
+#if RC_SIMT_ROT
+      // one step body (a third of the code of three ring phases, for the instruction cache):
+      // slot 0 = row q, 1 = row q+1, 2 = row q-1; the ring is rotated by register moves
+      for (int q = 0; q <= p.H; ++q) {
+        step<0>(b, q, gi, total);
+#pragma unroll
+        for (int r = 0; r < RPB; ++r)
+#pragma unroll
+          for (int k = 0; k < SW / 2; ++k) {
+            Y2[2][r][k] = Y2[0][r][k];
+            Y2[0][r][k] = Y2[1][r][k];
+          }
+      }
+#else
       for (int q0 = 0; q0 <= p.H; q0 += 3) {
         step<0>(b, q0, gi, total);
         if (q0 + 1 <= p.H) step<1>(b, q0 + 1, gi, total);
         if (q0 + 2 <= p.H) step<2>(b, q0 + 2, gi, total);
       }
+#endif
     }
     cp_async_wait<0>();
   }

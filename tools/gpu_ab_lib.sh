@@ -6,5 +6,5 @@ O=gpurun_out/ab_lib; mkdir -p $O; : > $O/summary.txt
 for rep in 1 2 3; do for w in $WLS; do for p in $PRECS; do for l in $LIBS; do
   RC_LIB_VARIANT=$PWD/$l timeout 300 python bench.py --workload $w --steps 20 --warmup 3 --no-cpu-baseline --no-cudnn \
     --precision $p --e2e-steps 1 > $O/b.json 2> $O/b.err
-  python -c "import json; d=json.loads(open('$O/b.json').read().strip().splitlines()[-1]); print('$rep $w $p $l kernel_ms=%.4f step_ms=%.4f' % (d['roofline']['kernel_ms'], d['ms_per_step']))" >> $O/summary.txt 2>&1
+  python -c "import json; d=json.loads(open('$O/b.json').read().strip().splitlines()[-1]); print('$rep $w $p $l kernel_ms=%s step_ms=%.4f layers=%s' % (d['roofline'].get('kernel_ms'), d['ms_per_step'], d.get('layer_ms')))" >> $O/summary.txt 2>&1
 done; done; done; done
