@@ -56,6 +56,13 @@ using namespace tc;
 #define RC_TC_TSA 0
 #endif
 constexpr bool kTsa = RC_TC_TSA != 0;
+// Experiment: bf16x3 for 16-wide images as 2 MMAs per K-step: Wh x [Xh; Xl] (N = 192, D
+// columns 0-95 = Wh Xh, 96-191 = Wh Xl) and Wl x Xh (N = 96, into columns 0-95); the
+// epilogue adds the two halves.  A third fewer MMA instructions, a third fewer weight reads.
+#ifndef RC_TC_CONCAT
+#define RC_TC_CONCAT 0
+#endif
+constexpr bool kConcat = RC_TC_CONCAT != 0;
 constexpr uint32_t A_COL0 = 448;  // TMEM columns [448, 512): two Ah regions
 
 template <int TW>
@@ -72,10 +79,13 @@ struct Geo {
   // D buffers from column D0.  Columns [0, D0) keep the 1-column-left halo load of a band's
   // first pixel inside the allocation; full-row bands also read their skipped (out-of-image)
   // window rows from them as zeros (band_rows), so they need D0 >= 18.
-  static constexpr uint32_t D0 = (STRIP || SMALL) ? 16 : 32;
+  static constexpr bool CAT = kConcat && TW == 16;          // D buffer = [hi 96 | lo 96]
+  static constexpr uint32_t D0 = CAT ? 0 : ((STRIP || SMALL) ? 16 : 32);
   // bf16x3 with Ah staged in TMEM (kTsa) keeps 2 x 32 columns at the top for it
   static constexpr uint32_t TOP = kTsa ? 64 : 0;
-  static constexpr int NDB = MMA_N * 5 + D0 + TOP <= 512 ? 5 : (MMA_N * 4 + D0 + TOP <= 512 ? 4 : 3);  // D buffers
+  static constexpr int DCOLS = CAT ? 2 * MMA_N : MMA_N;     // TMEM columns per D buffer
+  static constexpr int NDB = DCOLS * 5 + D0 + TOP <= 512 ? 5
+                             : (DCOLS * 4 + D0 + TOP <= 512 ? 4 : (DCOLS * 3 + D0 + TOP <= 512 ? 3 : 2));
   static constexpr int TR = SMALL ? 16 / TW : 1;              // output rows per epilogue thread
   static constexpr int IMGS = SMALL ? 64 / (TW * TW) : 1;     // images per band
 };
@@ -362,6 +372,18 @@ __device__ __forceinline__ void small_row(uint32_t a, int o0, float (&Y)[RPB][XH
   scatter_small<TW, RPB, CONV, T, I>(Y, z);
 }
 
+// concatenated bf16x3 (Geo::CAT): window row I = hi half + lo half of the D buffer
+template <int TW, int RPB, int CONV, int T, int I>
+__device__ __forceinline__ void cat_row(uint32_t a, float (&Y)[RPB][XH]) {
+  float z[18], t[16];
+  tmem_ld16(a + I * 16, *reinterpret_cast<float(*)[16]>(&z[1]));
+  tmem_ld16(a + Geo<TW>::MMA_N + I * 16, t);
+  tmem_wait_ld();
+#pragma unroll
+  for (int j = 0; j < 16; ++j) z[1 + j] += t[j];
+  scatter_row<TW, RPB, CONV, T, I>(Y, z);
+}
+
 struct EpiState {
   uint32_t row_base;  // TMEM address of D-buffer 0, first input row of the thread, its columns
   int db;
@@ -371,13 +393,14 @@ struct EpiState {
   int o0;              // small images: first output row of the thread (within its image)
   int vmask;           // window rows 0..2 inside the image (bit I); the others were not computed
   uint32_t zero_addr;  // TMEM columns [0, D0) of the thread's lane: zeros (full-row bands)
+  int cat;             // concatenated bf16x3 D buffers (Geo::CAT, resident X)
 };
 
 // one tap (compile-time T): three single-row TMEM round trips, D released after the last
 template <int TW, int RPB, int CONV, int T, bool PAIR>
 __device__ __forceinline__ void epi_tap(EpiState& e, float (&Y)[RPB][XH], uint64_t* d_full, uint64_t* d_empty) {
   constexpr int NDB = Geo<TW>::NDB;
-  const uint32_t a = e.row_base + e.db * Geo<TW>::MMA_N;
+  const uint32_t a = e.row_base + e.db * Geo<TW>::DCOLS;
   float z[18];
   if constexpr (PAIR)
     mbar_wait_spin(&d_full[e.db], e.dph);  // pairs: arrived by the leader's multicast commit
@@ -407,6 +430,27 @@ __device__ __forceinline__ void epi_tap(EpiState& e, float (&Y)[RPB][XH], uint64
     return;
   }
   // window rows outside the image were not computed (band_rows): read the zero columns
+  if constexpr (Geo<TW>::CAT) {
+    if (e.cat) {  // D = [Wh Xh + Wl Xh | Wh Xl]: each window row is the sum of both halves
+      cat_row<TW, RPB, CONV, T, 0>(a, Y);
+      cat_row<TW, RPB, CONV, T, 1>(a, Y);
+      float z[18], t[16];
+      tmem_ld16(a + 2 * 16, *reinterpret_cast<float(*)[16]>(&z[1]));
+      tmem_ld16(a + Geo<TW>::MMA_N + 2 * 16, t);
+      tmem_wait_ld();
+      tc_fence_before();
+      __syncwarp();
+      if (e.lane == 0) mbar_arrive(&d_empty[e.db]);
+      if (++e.db == NDB) {
+        e.db = 0;
+        e.dph ^= 1;
+      }
+#pragma unroll
+      for (int j = 0; j < 16; ++j) z[1 + j] += t[j];
+      scatter_row<TW, RPB, CONV, T, 2>(Y, z);
+      return;
+    }
+  }
   const int m = e.vmask;
   {  // rows 0 and 1 in flight together: one TMEM round trip instead of two
     float z1[18];
@@ -458,7 +502,7 @@ __device__ __forceinline__ Work make_work(const TcParams& p) {
 template <int TW, int RPB, int CONV, bool PAIR>
 __device__ void epilogue(const TcParams& p, uint32_t tmem, uint64_t* d_full, uint64_t* d_empty) {
   using G = Geo<TW>;
-  constexpr bool TRIM = !G::STRIP && !G::SMALL && !PAIR;  // see band_rows
+  constexpr bool TRIM = !G::STRIP && !G::SMALL && !PAIR && !G::CAT;  // see band_rows
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int q = warp % 4;
   const int sub = (warp - EPI_WARP0) / 4;
@@ -469,7 +513,8 @@ __device__ void epilogue(const TcParams& p, uint32_t tmem, uint64_t* d_full, uin
   const int o0 = G::SMALL ? (G::IMGS > 1 ? 0 : sub * G::TR) : 0;
   const uint32_t rb = G::SMALL ? (uint32_t)((s_img * TW + o0) * G::RS) : (uint32_t)(srow * G::RS + half * 16);
   EpiState e{tmem + ((uint32_t)(q * 32) << 16) + G::D0 + rb, 0, 0, lane, half,
-             PAIR ? mapa_shared(d_empty, 0) : 0u, o0, 7, tmem + ((uint32_t)(q * 32) << 16) + 1};
+             PAIR ? mapa_shared(d_empty, 0) : 0u, o0, 7, tmem + ((uint32_t)(q * 32) << 16) + 1,
+             (G::CAT && !PAIR && p.passes == 3 && !p.xstream) ? 1 : 0};
   if constexpr (TRIM) tmem_zero32(tmem + ((uint32_t)(q * 32) << 16));  // every warp of the quadrant
                                                                         // writes the same zeros
   const int nstrip = G::STRIP ? p.W / 16 : 1;
@@ -546,7 +591,7 @@ struct Ring {
 template <int TW, int RPB, int CONV, bool PAIR>
 __global__ void __launch_bounds__(THREADS, 1) ri_tc_kernel(const __grid_constant__ TcParams p) {
   using G = Geo<TW>;
-  constexpr bool TRIM = !G::STRIP && !G::SMALL && !PAIR;  // see band_rows
+  constexpr bool TRIM = !G::STRIP && !G::SMALL && !PAIR && !G::CAT;  // see band_rows
   constexpr int NDB = G::NDB;
   constexpr int XTILE = G::XTILE;                     // bytes of a full band tile (global layout)
   constexpr int XS = PAIR ? XTILE / 2 : XTILE;        // bytes of this CTA's part of it in smem
@@ -626,8 +671,13 @@ __global__ void __launch_bounds__(THREADS, 1) ri_tc_kernel(const __grid_constant
                 }
                 if (elect_one()) {
                   mbar_arrive_expect_tx(&x_full[c], parts * XS);
-                  bulk_g2s(xs + c * XS, p.xh + (tile + c) * XTILE + xoff, XS, &x_full[c]);
-                  if (parts == 2) bulk_g2s(xs + (p.NC + c) * XS, p.xl + (tile + c) * XTILE + xoff, XS, &x_full[c]);
+                  if (G::CAT && !PAIR && parts == 2) {  // [Xh_c | Xl_c]: one N = 192 B operand
+                    bulk_g2s(xs + 2 * c * XS, p.xh + (tile + c) * XTILE + xoff, XS, &x_full[c]);
+                    bulk_g2s(xs + (2 * c + 1) * XS, p.xl + (tile + c) * XTILE + xoff, XS, &x_full[c]);
+                  } else {
+                    bulk_g2s(xs + c * XS, p.xh + (tile + c) * XTILE + xoff, XS, &x_full[c]);
+                    if (parts == 2) bulk_g2s(xs + (p.NC + c) * XS, p.xl + (tile + c) * XTILE + xoff, XS, &x_full[c]);
+                  }
                 }
                 __syncwarp();
               }
@@ -717,7 +767,7 @@ __global__ void __launch_bounds__(THREADS, 1) ri_tc_kernel(const __grid_constant
                 mbar_wait(&d_empty[db], dph ^ 1);
             }
             tc_fence_after();
-            const uint32_t d = tmem + G::D0 + db * G::MMA_N + doff_k;
+            const uint32_t d = tmem + G::D0 + db * G::DCOLS + doff_k;
             for (int sp = 0; sp < stages_per_tap; ++sp) {
               if (t == 0 && b == 0 && !p.xstream)
                 for (int cl = 0; cl < p.spc; ++cl) {
@@ -732,11 +782,20 @@ __global__ void __launch_bounds__(THREADS, 1) ri_tc_kernel(const __grid_constant
                 for (int cl = 0; cl < ((p.ablate == 2 || p.ablate == 3) ? 0 : p.spc); ++cl) {
                   const int c = sp * p.spc + cl;
                   // X chunk: resident band tile c, or the stage's streamed copy
-                  const uint32_t xh_a = p.xstream ? wbase + stage_w + cl * XS : xaddr + c * XS;
-                  const uint32_t xl_a = p.xstream ? wbase + stage_w + (p.spc + cl) * XS : xaddr + (p.NC + c) * XS;
+                  const bool cat = G::CAT && !PAIR && parts == 2 && !p.xstream;
+                  const uint32_t xh_a = p.xstream ? wbase + stage_w + cl * XS : (cat ? xaddr + 2 * c * XS : xaddr + c * XS);
+                  const uint32_t xl_a = p.xstream ? wbase + stage_w + (p.spc + cl) * XS
+                                                  : (cat ? xaddr + (2 * c + 1) * XS : xaddr + (p.NC + c) * XS);
                   const uint64_t bh = desc_k_sw128(xh_a + xoff_k);
                   const uint64_t ah = desc_k_sw128(wbase + cl * parts * WTILE);
-                  if (kTsa && !PAIR && parts == 2) {
+                  if (G::CAT && !PAIR && cat) {
+                    const uint32_t idesc2 = idesc_bf16_f32(128, 2 * G::MMA_N);
+                    const uint64_t al = desc_k_sw128(wbase + (cl * parts + 1) * WTILE);
+#pragma unroll
+                    for (int kk = 0; kk < 4; ++kk) mma_bf16_ss(d, ah + 2 * kk, bh + 2 * kk, idesc2, (c | kk) != 0);
+#pragma unroll
+                    for (int kk = 0; kk < 4; ++kk) mma_bf16_ss(d, al + 2 * kk, bh + 2 * kk, idesc_k, 1);
+                  } else if (kTsa && !PAIR && parts == 2) {
                     const uint32_t atm = tmem + A_COL0 + (areg++ & 1) * 32;
 #pragma unroll
                     for (int kk = 0; kk < 4; ++kk) tmem_cp_128x256b(atm + 8 * kk, ah + 2 * kk);
