@@ -59,16 +59,16 @@ __global__ void pool_backward_kernel(const float* __restrict__ gy, const uint8_t
 
 // the same, 4 pixels per thread (plane % 4 == 0): one index decode per float4, 128-bit
 // loads / stores, uchar4 argmax reads
+template <typename IT>  // index type: 32-bit division when the tensor allows it
 __global__ void pool_backward_vec_kernel(const float4* __restrict__ gy, const uchar4* __restrict__ am,
                                          float4* __restrict__ df, long long planes_nc, int R, int RO, int plane4,
                                          int pool, int gf, float inv_r) {
-  const long long total = planes_nc * R * plane4;
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
-       i += (long long)gridDim.x * blockDim.x) {
-    const long long pi = i / plane4;  // (nc, o) plane
-    const int px = (int)(i - pi * plane4);
-    const int o = (int)(pi % R);
-    const long long nc = pi / R;
+  const IT total = (IT)(planes_nc * R * plane4);
+  for (IT i = blockIdx.x * (IT)blockDim.x + threadIdx.x; i < total; i += (IT)gridDim.x * blockDim.x) {
+    const IT pi = i / (IT)plane4;  // (nc, o) plane
+    const int px = (int)(i - pi * (IT)plane4);
+    const int o = (int)(pi % (IT)R);
+    const long long nc = (long long)(pi / (IT)R);
     float4 v;
     if (pool == RC_POOL_NONE) {
       v = gy[(nc * RO + o) * plane4 + px];
@@ -225,9 +225,16 @@ int launch_pool_backward(const rc_desc& d, const float* gy, const uint8_t* am, f
   if (work == 0) return RC_OK;
   const bool pow2 = (R & (R - 1)) == 0;  // x / R == x * (1/R) exactly
   if (plane % 4 == 0 && (d.pool != RC_POOL_AVG || pow2))
-    pool_backward_vec_kernel<<<grid_for(work / 4, 256), 256, 0, s>>>(
-        reinterpret_cast<const float4*>(gy), reinterpret_cast<const uchar4*>(am), reinterpret_cast<float4*>(df),
-        (long long)d.n * d.c_out, R, RO, plane / 4, d.pool, pool_fold(d), 1.0f / (float)R);
+  {
+    if (work / 4 < (1LL << 31))
+      pool_backward_vec_kernel<unsigned><<<grid_for(work / 4, 256), 256, 0, s>>>(
+          reinterpret_cast<const float4*>(gy), reinterpret_cast<const uchar4*>(am), reinterpret_cast<float4*>(df),
+          (long long)d.n * d.c_out, R, RO, plane / 4, d.pool, pool_fold(d), 1.0f / (float)R);
+    else
+      pool_backward_vec_kernel<unsigned long long><<<grid_for(work / 4, 256), 256, 0, s>>>(
+          reinterpret_cast<const float4*>(gy), reinterpret_cast<const uchar4*>(am), reinterpret_cast<float4*>(df),
+          (long long)d.n * d.c_out, R, RO, plane / 4, d.pool, pool_fold(d), 1.0f / (float)R);
+  }
   else
     pool_backward_kernel<<<grid_for(work, 256), 256, 0, s>>>(gy, am, df, (long long)d.n * d.c_out, R, RO, plane,
                                                             d.pool, pool_fold(d));

@@ -56,19 +56,19 @@ __device__ __forceinline__ void split_bf16(float v, __nv_bfloat16& hi, __nv_bflo
 // G [n][M][H][W] fp32 -> Gp[mt][kc][part][128 m][64 q] over the padded pixel grid (pads 0).
 // Thread = (m, kc, 8-q group): 8 threads fill one 128-byte row; a warp reads 256
 // consecutive q of one m (coalesced), decoding (n, h, w) once and stepping after that.
+template <typename IT>  // index type: 32-bit divisions when the packed G allows it
 __global__ void __launch_bounds__(256) g_pack_kernel(const float* __restrict__ g, uint8_t* __restrict__ gp, int M,
                                                      int MT, int KC, int H, int W, int Wp, int Pimg, long long QN,
                                                      int parts) {
-  const long long total = (long long)MT * 128 * KC * 8;
+  const IT total = (IT)((long long)MT * 128 * KC * 8);
   const size_t plane = (size_t)H * W;
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
-       i += (long long)gridDim.x * blockDim.x) {
+  for (IT i = blockIdx.x * (IT)blockDim.x + threadIdx.x; i < total; i += (IT)gridDim.x * blockDim.x) {
     const int grp = (int)(i % 8);
-    const long long kc = (i / 8) % KC;
-    const long long m = i / (8LL * KC);
+    const IT kc = (i / 8) % (IT)KC;
+    const IT m = i / (8 * (IT)KC);
     const int mt = (int)(m / 128), ml = (int)(m % 128);
-    long long q = kc * KQ + grp * 8;
-    int n = (int)(q / Pimg), rem = (int)(q - (long long)n * Pimg);
+    const IT q = kc * KQ + grp * 8;
+    int n = (int)(q / (IT)Pimg), rem = (int)(q - (IT)n * (IT)Pimg);
     int hp = rem / Wp, wp = rem - hp * Wp;
     // addresses first (the pixel walk is sequential), then 8 independent loads in flight
     long long src[8];
@@ -331,7 +331,11 @@ int launch_wgrad(const rc_desc& d, const float* x, const float* df, float* dF, v
   {
     const long long total = (long long)g.MT * 128 * g.KC * 8;
     const long long grid = total / 256 + 1 < 148 * 32 ? total / 256 + 1 : 148 * 32;
-    g_pack_kernel<<<(int)grid, 256, 0, s>>>(df, gp, g.M, g.MT, g.KC, d.h, d.w, pg.Wp, pg.Pimg, g.QN, g.parts);
+    if (total < (1LL << 31) && g.QN + KQ < (1LL << 31))
+      g_pack_kernel<unsigned><<<(int)grid, 256, 0, s>>>(df, gp, g.M, g.MT, g.KC, d.h, d.w, pg.Wp, pg.Pimg, g.QN, g.parts);
+    else
+      g_pack_kernel<unsigned long long><<<(int)grid, 256, 0, s>>>(df, gp, g.M, g.MT, g.KC, d.h, d.w, pg.Wp, pg.Pimg,
+                                                                  g.QN, g.parts);
     RC_CUDA(cudaGetLastError());
   }
   WgParams p;
