@@ -134,12 +134,6 @@ __device__ __forceinline__ void tmem_ld8(uint32_t taddr, float* v) {
 #pragma unroll
   for (int i = 0; i < 8; ++i) v[i] = __uint_as_float(r[i]);
 }
-__device__ __forceinline__ void tmem_ld2(uint32_t taddr, float* v) {
-  uint32_t r[2];
-  asm volatile("tcgen05.ld.sync.aligned.32x32b.x2.b32 {%0,%1}, [%2];\n" : "=r"(r[0]), "=r"(r[1]) : "r"(taddr));
-  v[0] = __uint_as_float(r[0]);
-  v[1] = __uint_as_float(r[1]);
-}
 
 // ---- pooling epilogue ------------------------------------------------------------------
 // max-fold of rotations [R0, R0+G) of this base into Yr[R0] (+ argmax, ties -> smallest
@@ -364,10 +358,11 @@ __device__ __forceinline__ void small_row(uint32_t a, int o0, float (&Y)[RPB][XH
   const int row = o0 - 1 + I;  // image row of window row I
   if (row < 0 || row >= TW) return;  // the zero padding (warp-uniform)
   float z[10];
+  const uint32_t ra = a + (uint32_t)(I * TW) - (uint32_t)TW;  // window row I = image row o0 - 1 + I
   if constexpr (TW == 8)
-    tmem_ld8(a + (I - 1) * TW, z + 1);
+    tmem_ld8(ra, z + 1);
   else
-    tmem_ld4(a + (I - 1) * TW, z + 1);
+    tmem_ld4(ra, z + 1);
   tmem_wait_ld();
   scatter_small<TW, RPB, CONV, T, I>(Y, z);
 }

@@ -74,8 +74,8 @@ __global__ void __launch_bounds__(256) g_pack_kernel(const float* __restrict__ g
     long long src[8];
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
-      src[j] = (m < M && q + j < QN && hp >= 1 && hp <= H && wp >= 1 && wp <= W)
-                   ? ((long long)n * M + m) * (long long)plane + (long long)(hp - 1) * W + (wp - 1)
+      src[j] = ((long long)m < M && (long long)q + j < QN && hp >= 1 && hp <= H && wp >= 1 && wp <= W)
+                   ? ((long long)n * M + (long long)m) * (long long)plane + (long long)(hp - 1) * W + (wp - 1)
                    : -1;
       if (++wp == Wp) {
         wp = 0;
