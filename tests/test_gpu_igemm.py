@@ -28,6 +28,7 @@ CONFIGS = [
     (5, 256, 8, 12, 96, "raw", "none", "none"),
     (1, 200, 1, 1, 200, "scatter", "none", "none"),
     (2, 24, 3, 70, 33, "scatter", "max", "relu"),
+    (2, 1100, 6, 10, 72, "scatter", "max", "relu"),   # 3 accumulation segments (8 ci chunks each)
 ]
 
 
