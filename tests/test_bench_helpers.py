@@ -1,0 +1,42 @@
+"""bench.py helpers that shape the JSON contract (CPU only: no kernel is launched)."""
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+
+def test_smem_traffic_c3_geometry():
+    import bench
+    import paper_2512_08888_b200 as P
+    d = P.Desc(256, 256, 16, 16, 1024, 3, "steer", 8, "subgroup", 4, "scatter", "auto")
+    b = bench.smem_traffic(d, "tc_k3w16_bf16x3")
+    # per item: bands N = 80, 96, 96, 80 (edge bands trimmed); K-step = 3*4096 + 3*N*32 + 2*4096
+    per_kstep = lambda n: 3 * 4096 + 3 * n * 32 + 2 * 4096
+    per_item = sum(2 * 9 * 4 * 4 * per_kstep(n) + 2 * 4 * n * 128 for n in (80, 96, 96, 80))
+    assert b == per_item * 256 * 8
+    assert 68e9 < b < 70e9
+    assert bench.smem_traffic(d, "simt_k3<8,2,4>") is None
+    one = bench.smem_traffic(d, "tc_k3w16_bf16")
+    assert one < b / 2  # one pass: 1 A + 1 B read and 1 weight part per K-step
+
+
+def test_smem_roofline_fields():
+    import bench
+    import paper_2512_08888_b200 as P
+    d = P.Desc(256, 256, 16, 16, 1024, 3, "steer", 8, "subgroup", 4, "scatter", "auto")
+    if not d.kernel_name().startswith("tc_"):  # CPU container: the dispatcher answers without a GPU
+        assert bench.smem_roofline(d, 2.35) is None or bench.smem_roofline(d, 2.35)["unit"] == "TB/s"
+        return
+    r = bench.smem_roofline(d, 2.35)
+    assert r["unit"] == "TB/s" and abs(r["peak"] - 37.2) < 0.1 and 0.7 < r["frac"] < 0.85
+
+
+def test_clock_sampler_unsampled_summary():
+    import bench
+    c = bench.ClockSampler(0)
+    s = c.summary()
+    assert s["reasons"] == ["unsampled"] and s["samples"] == 0
+    c.rows.append((1965.0, 1965.0, ["Not Active", "Not Active", "Not Active", "Active"]))
+    s = c.summary()
+    assert s["sm_mhz"] == 1965.0 and s["reasons"] == ["sw_power_cap"] and s["samples"] == 1
