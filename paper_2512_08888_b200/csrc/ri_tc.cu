@@ -776,15 +776,19 @@ __global__ void __launch_bounds__(THREADS, 1) ri_tc_kernel(const __grid_constant
               tc_fence_after();
               if (elect_one()) {
                 const uint32_t wbase = smem_u32(ws + wr.s * stage_bytes);
+                // descriptors are linear in the smem address (14-bit field, smem < 256 KB): one
+                // base per stage, constant strides per chunk (with the 64-register MMA warp this
+                // denser issue is 1% faster; at 32 registers it was 8-12% slower)
+                const bool cat = G::CAT && !PAIR && parts == 2 && !p.xstream;
+                const uint32_t xstride = cat ? 2 * XS : XS;  // X chunk c: resident band tile or the stage's copy
+                const uint32_t xbase = p.xstream ? wbase + stage_w : xaddr + sp * p.spc * xstride;
+                const uint32_t lo_off = cat ? XS : (p.xstream ? p.spc * XS : p.NC * XS);
+                const uint64_t b0 = desc_k_sw128(xbase + xoff_k), a0 = desc_k_sw128(wbase);
                 for (int cl = 0; cl < ((p.ablate == 2 || p.ablate == 3) ? 0 : p.spc); ++cl) {
                   const int c = sp * p.spc + cl;
-                  // X chunk: resident band tile c, or the stage's streamed copy
-                  const bool cat = G::CAT && !PAIR && parts == 2 && !p.xstream;
-                  const uint32_t xh_a = p.xstream ? wbase + stage_w + cl * XS : (cat ? xaddr + 2 * c * XS : xaddr + c * XS);
-                  const uint32_t xl_a = p.xstream ? wbase + stage_w + (p.spc + cl) * XS
-                                                  : (cat ? xaddr + (2 * c + 1) * XS : xaddr + (p.NC + c) * XS);
-                  const uint64_t bh = desc_k_sw128(xh_a + xoff_k);
-                  const uint64_t ah = desc_k_sw128(wbase + cl * parts * WTILE);
+                  const uint32_t xh_a = xbase + cl * xstride, xl_a = xh_a + lo_off;
+                  const uint64_t bh = b0 + (uint32_t)((cl * xstride) >> 4);
+                  const uint64_t ah = a0 + (uint32_t)((cl * parts * WTILE) >> 4);
                   if (G::CAT && !PAIR && cat) {
                     const uint32_t idesc2 = idesc_bf16_f32(128, 2 * G::MMA_N);
                     const uint64_t al = desc_k_sw128(wbase + (cl * parts + 1) * WTILE);

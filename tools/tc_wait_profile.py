@@ -1,4 +1,5 @@
-"""Where the band kernel's MMA warp waits (RC_TC_ABLATE=10 instrumentation, ri_tc.cu):
+"""Where the band kernel's MMA warp waits (RC_TC_ABLATE=10 instrumentation; the clock64 patch
+for ri_tc.cu is not in the tree, see profiles/r01/regsplit_ab.txt):
 per CTA, total cycles of the MMA warp and the cycles spent waiting for a free TMEM D buffer
 (epilogue), for the X band (TMA) and for a weight stage (TMA).  Outputs are overwritten.
 
