@@ -32,7 +32,7 @@
 namespace rc {
 namespace {
 
-constexpr int CC = 16;  // input channels per shared-memory stage
+constexpr int CC = 32;  // input channels per shared-memory stage (32: half the CTA barriers of 16, C3 fp32 -5.6%)
 
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool valid) {
   const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
