@@ -63,6 +63,10 @@ constexpr bool kTsa = RC_TC_TSA != 0;
 #define RC_TC_CONCAT 0
 #endif
 constexpr bool kConcat = RC_TC_CONCAT != 0;
+#ifndef RC_TC_ROWBYROW
+#define RC_TC_ROWBYROW 1
+#endif
+constexpr bool kRowByRow = RC_TC_ROWBYROW != 0;  // epilogue loads one window row at a time
 constexpr uint32_t A_COL0 = 448;  // TMEM columns [448, 512): two Ah regions
 
 template <int TW>
@@ -449,7 +453,15 @@ __device__ __forceinline__ void epi_tap(EpiState& e, float (&Y)[RPB][XH], uint64
     }
   }
   const int m = e.vmask;
-  {  // rows 0 and 1 in flight together: one TMEM round trip instead of two
+  if constexpr (kRowByRow && TW == 16) {
+    // one window row at a time: a TMEM round trip is ~22 cycles, and a single 16-value row
+    // in flight keeps the epilogue's registers (Y = 64) clear of spills, which would share
+    // the L1/shared-memory bandwidth the SS MMAs are bound by
+    load_row<TW>((m & 1) ? a : e.zero_addr, e.half, z);
+    scatter_row<TW, RPB, CONV, T, 0>(Y, z);
+    load_row<TW>((m & 2) ? a + Geo<TW>::RS : e.zero_addr, e.half, z);
+    scatter_row<TW, RPB, CONV, T, 1>(Y, z);
+  } else {  // rows 0 and 1 in flight together: one TMEM round trip instead of two
     float z1[18];
     if (TW == 16 && (m & 3) == 3) {
       tmem_ld_rows2(a, z, z1);
