@@ -9,9 +9,13 @@
 // * Errors: the C-ABI returns status codes.  RC_ERR_INVALID becomes std::invalid_argument
 //   with the reference's message (e.g. "tiled_scatter_conv: invalid halo",
 //   scatter_conv.hpp:345); every other failure becomes std::runtime_error.
-// * Arithmetic: the ops compute in float32 on the GPU (the reference's benchmark mode,
-//   tensor.hpp:16-17).  Instantiating a GPU op with T = double is a compile-time error --
-//   there is no CPU fallback in the product.
+// * Arithmetic: the ops take float32 in and out (the reference's benchmark mode,
+//   tensor.hpp:16-17).  The channel contraction runs in the per-thread default precision
+//   (rotconv::b200::precision(), default Precision::automatic = the FP32-tolerance
+//   tcgen05 kernels where a shape has one, FP32 CUDA cores otherwise); set it with
+//   set_precision() or scope it with PrecisionScope (e.g. Precision::fp32 for the
+//   CUDA-core FFMA path).  Instantiating a GPU op with T = double is a compile-time
+//   error -- there is no CPU fallback in the product.
 #pragma once
 
 #include <stdexcept>
@@ -43,6 +47,26 @@ class DeviceScope {
 
 // precision of the channel contraction for the fused layer (rc_precision)
 enum class Precision { automatic = RC_PREC_AUTO, fp32 = RC_PREC_FP32, bf16x3 = RC_PREC_BF16X3, bf16 = RC_PREC_BF16 };
+
+// per-thread default precision of the reference-signature drop-ins (scatter_conv.hpp,
+// group_conv.hpp), which have no precision argument
+inline Precision& current_precision_slot() {
+  thread_local Precision p = Precision::automatic;
+  return p;
+}
+inline Precision precision() { return current_precision_slot(); }
+inline void set_precision(Precision p) { current_precision_slot() = p; }
+
+class PrecisionScope {
+ public:
+  explicit PrecisionScope(Precision p) : prev_(precision()) { set_precision(p); }
+  ~PrecisionScope() { set_precision(prev_); }
+  PrecisionScope(const PrecisionScope&) = delete;
+  PrecisionScope& operator=(const PrecisionScope&) = delete;
+
+ private:
+  Precision prev_;
+};
 
 inline void throw_on(int status) {
   if (status == RC_OK) return;

@@ -137,7 +137,7 @@ OrientedFeature<T> group_conv(const Tensor3<T>& x, const FilterBank<T>& w, const
   detail::check(x.channels() == w.in_channels(), "group_conv: channel mismatch");
   detail::check(w.square() && w.kernel_h() % 2 == 1, "transform_kernel: rotation groups need odd square kernels");
   const rc_desc d = group_desc(1, x.channels(), x.height(), x.width(), w.out_channels(), w.kernel_h(), group_code(g),
-                               g.size(), Pooling::none, 1, convention, b200::Precision::fp32);
+                               g.size(), Pooling::none, 1, convention, b200::precision());
   OrientedFeature<T> f(w.out_channels(), g.size(), x.height(), x.width());
   b200::throw_on(rc_ri_conv_forward_host(&d, x.data(), w.data(), nullptr, nullptr, f.data(), nullptr, b200::device()));
   if (counter) {  // one channel dot per (h,w,co,m,n) per base, |G|-independent
@@ -345,7 +345,7 @@ struct RILayerSpec {
   Pooling pool = Pooling::subgroup;
   int pool_group = 4;
   int convention = RC_CONV_SCATTER;
-  b200::Precision precision = b200::Precision::fp32;
+  b200::Precision precision = b200::Precision::automatic;
   int activation = RC_ACT_NONE;  // RC_ACT_RELU fuses a ReLU after the bias
 
   int out_orientations() const {

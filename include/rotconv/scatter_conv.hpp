@@ -40,7 +40,8 @@ struct MultCounter {
   void reset() { scalar_multiplications = scalar_additions = 0; }
 };
 
-// high-water mark of auxiliary bytes; here: the device workspace a call stages through
+// high-water mark of auxiliary bytes, with the reference's accounting (:351-360): the
+// private tile accumulators of tile_private (tile_h * tile_w * sizeof(T) * workers)
 struct AuxMemCounter {
   std::size_t current_bytes = 0;
   std::size_t peak_bytes = 0;
@@ -94,7 +95,7 @@ inline rc_desc single_desc(int n, int cin, int h, int w, int cout, int k, int co
   d.pool = RC_POOL_NONE;
   d.pool_group = 1;
   d.convention = convention;
-  d.precision = RC_PREC_FP32;
+  d.precision = static_cast<int>(b200::precision());
   return d;
 }
 
@@ -187,7 +188,7 @@ Tensor3<T> tiled_scatter_conv(const Tensor3<T>& x, const FilterBank<T>& w, const
                                             w.out_channels(), w.in_channels(), w.kernel_h(), w.kernel_w(),
                                             cfg.tile_h, cfg.tile_w, cfg.halo, workers,
                                             static_cast<int>(strategy), y.data(), &mults, &adds, &aux_bytes,
-                                            b200::device()));
+                                            static_cast<int>(b200::precision()), b200::device()));
   if (aux && strategy == ScatterStrategy::tile_private) {
     aux->acquire(aux_bytes);
     aux->release(aux_bytes);

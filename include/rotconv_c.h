@@ -36,7 +36,7 @@
 extern "C" {
 #endif
 
-#define RC_ABI_VERSION 2
+#define RC_ABI_VERSION 3
 
 enum rc_status {
   RC_OK = 0,
@@ -190,13 +190,16 @@ int rc_mgpu_forward_host(const rc_desc* d, const float* h_x, const float* h_w0,
  * exactly like the reference (channel mismatch, square kernel, tile dims,
  * halo == K/2, workers >= 1) and returns the identical-semantics output for one
  * image.  tile/workers/strategy do not change the result (the reference is
- * bit-identical across them, scatter_conv.hpp:21-23).  mults/adds/aux_peak
- * (nullable) receive the MultCounter / AuxMemCounter increments. */
+ * bit-identical across them, scatter_conv.hpp:21-23).  mults/adds/aux_bytes
+ * (nullable) receive the MultCounter / AuxMemCounter increments with the reference's
+ * semantics: aux_bytes = tile_h*tile_w*sizeof(float)*workers for tile_private, 0 for
+ * phase_parallel (scatter_conv.hpp:351-360).  `precision` (rc_precision, ABI 3) selects
+ * the arithmetic; RC_PREC_AUTO (0) is the default of every drop-in. */
 int rc_tiled_scatter_conv_host(const float* h_x, int c_in, int h, int w, const float* h_wt,
                                int c_out, int in_channels_w, int kh, int kw, int tile_h,
                                int tile_w, int halo, int workers, int strategy, float* h_y,
                                unsigned long long* mults, unsigned long long* adds,
-                               unsigned long long* aux_bytes, int device);
+                               unsigned long long* aux_bytes, int precision, int device);
 
 #ifdef __cplusplus
 }

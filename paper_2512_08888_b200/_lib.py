@@ -9,8 +9,7 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-# RC_LIB_VARIANT: a same-box A/B of two builds of this library (tools/gpu_ab_lib.sh)
-LIB_PATH = os.environ.get("RC_LIB_VARIANT") or os.path.join(HERE, "librotconv_b200.so")
+LIB_PATH = os.path.join(HERE, "librotconv_b200.so")
 
 RC_OK, RC_ERR_INVALID, RC_ERR_CUDA, RC_ERR_UNSUPPORTED, RC_ERR_WORKSPACE = 0, -1, -2, -3, -4
 GROUPS = {"single": 0, "p4": 1, "p4m": 2, "steer": 3}
@@ -61,7 +60,7 @@ SIGNATURES = {
     "rc_gap_linear": (C.c_int, [C.c_int] * 4 + [_VP, _VP, _VP, C.c_int, _VP, _VP]),
     "rc_tiled_scatter_conv_host": (C.c_int, [_VP] + [C.c_int] * 3 + [_VP] + [C.c_int] * 9 +
                                    [_VP, _P(C.c_ulonglong), _P(C.c_ulonglong),
-                                    _P(C.c_ulonglong), C.c_int]),
+                                    _P(C.c_ulonglong), C.c_int, C.c_int]),
 }
 
 _lib = None

@@ -56,6 +56,9 @@ int validate(const rc_desc& d) {
     return fail(RC_ERR_INVALID, "Tensor3: dimensions must be positive");
   if (d.c_out < 1) return fail(RC_ERR_INVALID, "FilterBank: channel counts must be positive");
   if (d.k < 1) return fail(RC_ERR_INVALID, "FilterBank: kernel dims must be >= 1");
+  // every kernel and index table (tap maps, bank steering, backward tap offsets) is sized
+  // for kMaxK x kMaxK taps: refuse larger kernels before anything touches them
+  if (d.k > kMaxK) return fail(RC_ERR_UNSUPPORTED, "ri_conv: kernel size > 11 unsupported");
   switch (d.group) {
     case RC_GROUP_SINGLE:
       if (d.orientations != 1) return fail(RC_ERR_INVALID, "ri_conv: single group needs 1 orientation");
@@ -203,7 +206,6 @@ int dispatch(const rc_desc& d, const float* x, const void* bank, const float* bi
   int st = launch_simt_k3(d, x, bank, bias, y, am, s, dry, name);
   if (st != RC_ERR_UNSUPPORTED) return st;
   if (dry) {
-    if (d.k > kMaxK) return fail(RC_ERR_UNSUPPORTED, "ri_conv: kernel size > 11 unsupported");
     if (name) *name = "generic";
     return RC_OK;
   }
@@ -592,20 +594,23 @@ int rc_tiled_scatter_conv_host(const float* h_x, int c_in, int h, int w, const f
                                int c_out, int in_channels_w, int kh, int kw, int tile_h,
                                int tile_w, int halo, int workers, int strategy, float* h_y,
                                unsigned long long* mults, unsigned long long* adds,
-                               unsigned long long* aux_bytes, int device) {
-  (void)strategy;
+                               unsigned long long* aux_bytes, int precision, int device) {
   // scatter_conv.hpp:339-346, same order and messages
   if (c_in != in_channels_w) return fail(RC_ERR_INVALID, "tiled_scatter_conv: channel mismatch");
   if (kh != kw) return fail(RC_ERR_INVALID, "tiled_scatter_conv: kernel must be square");
   if (tile_h < 1 || tile_w < 1) return fail(RC_ERR_INVALID, "tiled_scatter_conv: tile dims must be >= 1");
   if (halo != kh / 2) return fail(RC_ERR_INVALID, "tiled_scatter_conv: invalid halo");
   if (workers < 1) return fail(RC_ERR_INVALID, "tiled_scatter_conv: workers must be >= 1");
-  rc_desc d{1, c_in, h, w, c_out, kh, RC_GROUP_SINGLE, 1, RC_POOL_NONE, 1, RC_CONV_SCATTER, RC_PREC_FP32, RC_ACT_NONE};
+  rc_desc d{1, c_in, h, w, c_out, kh, RC_GROUP_SINGLE, 1, RC_POOL_NONE, 1, RC_CONV_SCATTER, precision, RC_ACT_NONE};
   int st = rc_ri_conv_forward_host(&d, h_x, h_wt, nullptr, nullptr, h_y, nullptr, device);
   if (st != RC_OK) return st;
   if (mults) *mults = (unsigned long long)h * w * kh * kw * c_in * c_out;  // :361-366
   if (adds) *adds = rc_clipped_writes(h, w, kh, kw) * c_out;
-  if (aux_bytes) *aux_bytes = rc_workspace_size(&d);
+  // AuxMemCounter keeps the reference's accounting (:351-360): the per-worker private tile
+  // accumulators of tile_private, none for phase_parallel.  The GPU path's own staging is
+  // reported by rc_workspace_size.
+  if (aux_bytes)
+    *aux_bytes = strategy == 0 ? (unsigned long long)tile_h * tile_w * sizeof(float) * workers : 0ull;
   return RC_OK;
 }
 

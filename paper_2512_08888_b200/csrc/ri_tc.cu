@@ -207,6 +207,10 @@ __device__ __forceinline__ void finalize_row(const TcParams& p, float (&Yr)[RPB]
     if (b == p.NB - 1) {  // R is a power of two here (tc_supported): x * (1/R) == x / R exactly
 #pragma unroll
       for (int j = 0; j < XH; ++j) Yr[0][j] = __fadd_rn(__fmul_rn(Yr[0][j], p.inv_r), bz);
+      if (p.act == RC_ACT_RELU) {
+#pragma unroll
+        for (int j = 0; j < XH; ++j) Yr[0][j] = fmaxf(Yr[0][j], 0.f);
+      }
     }
     store8(p.y + ybase, Yr[0]);
     return;

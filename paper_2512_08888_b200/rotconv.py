@@ -113,7 +113,7 @@ class Desc:
     pool: str = "none"
     pool_group: int = 4
     convention: str = "scatter"
-    precision: str = "fp32"
+    precision: str = "auto"
     activation: str = "none"
 
     def c(self) -> rc_desc:
@@ -252,7 +252,7 @@ def ri_conv_forward(desc: Desc, x: torch.Tensor, bank: torch.Tensor,
 def ri_conv(x: torch.Tensor, w0: torch.Tensor, w1: torch.Tensor | None = None, *,
             group: str = "steer", orientations: int = 8, pool: str = "subgroup",
             pool_group: int = 4, bias: torch.Tensor | None = None, convention: str = "scatter",
-            precision: str = "fp32", counter: MultCounter | None = None):
+            precision: str = "auto", counter: MultCounter | None = None):
     """Whole RI layer (bank precompute + fused forward) on a batch (N,Cin,H,W)."""
     squeeze = x.dim() == 3
     xb = x.unsqueeze(0) if squeeze else x
@@ -278,7 +278,7 @@ class RIConv:
     """Stateful layer: weights + precomputed bank, reused across forwards."""
 
     def __init__(self, w0, w1=None, *, group="steer", orientations=8, pool="subgroup",
-                 pool_group=4, bias=None, convention="scatter", precision="fp32"):
+                 pool_group=4, bias=None, convention="scatter", precision="auto"):
         self.w0, self.w1, self.bias = w0, w1, bias
         self.kw = dict(group=group, orientations=orientations, pool=pool, pool_group=pool_group,
                        convention=convention, precision=precision)
@@ -288,10 +288,20 @@ class RIConv:
     def desc(self, n, h, w) -> Desc:
         return Desc(n, self.w0.shape[1], h, w, self.w0.shape[0], self.w0.shape[2], **self.kw)
 
+    def _weights_key(self):
+        # the bank depends only on the weight values (not on N, H or W): rebuild it when a
+        # weight tensor is replaced or updated in place (an optimizer step bumps _version)
+        return tuple((t.data_ptr(), t._version) if t is not None else None for t in (self.w0, self.w1))
+
+    def refresh_bank(self) -> None:
+        """Drop the cached bank; the next call rebuilds it from the current weights."""
+        self._bank = None
+        self._bank_key = None
+
     def __call__(self, x: torch.Tensor):
         n, _, h, w = x.shape
         desc = self.desc(n, h, w)
-        key = (h, w)
+        key = self._weights_key()
         if self._bank is None or self._bank_key != key:
             self._bank = bank_precompute(desc, self.w0, self.w1)
             self._bank_key = key
@@ -299,28 +309,38 @@ class RIConv:
 
 
 # ------------------------------------------------------------- reference-named operations
-def _single_desc(x: torch.Tensor, w: torch.Tensor, convention: str) -> tuple[Desc, torch.Tensor, bool]:
+# Precision of the reference-named drop-ins, which have no precision argument in the
+# reference signatures: "auto" (the FP32-tolerance tensor-core kernels where the shape has
+# one) unless the caller passes precision= explicitly (e.g. "fp32" for the CUDA-core FFMA
+# path, bit-identical to the reference on exactly representable inputs).
+DEFAULT_PRECISION = "auto"
+
+
+def _single_desc(x: torch.Tensor, w: torch.Tensor, convention: str,
+                 precision: str | None = None) -> tuple[Desc, torch.Tensor, bool]:
     squeeze = x.dim() == 3
     xb = x.unsqueeze(0) if squeeze else x
     n, cin, h, ww = xb.shape
-    return Desc(n, cin, h, ww, w.shape[0], w.shape[2], "single", 1, "none", 1, convention), xb, squeeze
+    return (Desc(n, cin, h, ww, w.shape[0], w.shape[2], "single", 1, "none", 1, convention,
+                 precision or DEFAULT_PRECISION), xb, squeeze)
 
 
-def _run_single(x, w, convention, name):
+def _run_single(x, w, convention, name, precision=None):
     if w.shape[1] != x.shape[-3]:
         raise ValueError(f"{name}: channel mismatch")
     if w.shape[2] != w.shape[3]:
         raise ValueError(f"{name}: kernel must be square")
-    desc, xb, squeeze = _single_desc(x, w, convention)
+    desc, xb, squeeze = _single_desc(x, w, convention, precision)
     bank = bank_precompute(desc, w)
     y, _ = ri_conv_forward(desc, xb, bank)
     y = y[:, :, 0]
     return y[0] if squeeze else y
 
 
-def scatter_conv_multi(x: torch.Tensor, w: torch.Tensor, counter: MultCounter | None = None):
+def scatter_conv_multi(x: torch.Tensor, w: torch.Tensor, counter: MultCounter | None = None, *,
+                       precision: str | None = None):
     """scatter_conv.hpp:189-193: equals conv_gather_same(x, reverse_bank(w))."""
-    y = _run_single(x, w, "scatter", "scatter_conv_multi")
+    y = _run_single(x, w, "scatter", "scatter_conv_multi", precision)
     if counter is not None:
         n = 1 if x.dim() == 3 else x.shape[0]
         h, ww = x.shape[-2:]
@@ -329,9 +349,10 @@ def scatter_conv_multi(x: torch.Tensor, w: torch.Tensor, counter: MultCounter | 
     return y
 
 
-def scatter_conv_raw_multi(x: torch.Tensor, w: torch.Tensor, counter: MultCounter | None = None):
+def scatter_conv_raw_multi(x: torch.Tensor, w: torch.Tensor, counter: MultCounter | None = None, *,
+                           precision: str | None = None):
     """scatter_conv.hpp:151-187: raw scatter indices, equals conv_gather_same(x, w)."""
-    y = _run_single(x, w, "raw", "scatter_conv_multi")
+    y = _run_single(x, w, "raw", "scatter_conv_multi", precision)
     if counter is not None:
         n = 1 if x.dim() == 3 else x.shape[0]
         h, ww = x.shape[-2:]
@@ -340,14 +361,15 @@ def scatter_conv_raw_multi(x: torch.Tensor, w: torch.Tensor, counter: MultCounte
     return y
 
 
-def scatter_conv_single(x: torch.Tensor, k: torch.Tensor, counter: MultCounter | None = None):
+def scatter_conv_single(x: torch.Tensor, k: torch.Tensor, counter: MultCounter | None = None, *,
+                        precision: str | None = None):
     """scatter_conv.hpp:143-149: single plane (H,W) with an arbitrary (Kh,Kw) kernel."""
     if k.shape[0] != k.shape[1]:
         # the reference supports rectangular single-plane kernels; the GPU kernels
         # are square-only, so refuse rather than silently differ
         raise ValueError("scatter_conv_single: kernel must be square on the GPU path")
     y = _run_single(x.reshape(1, 1, *x.shape), k.reshape(1, 1, *k.shape), "scatter",
-                    "scatter_conv_single")[0, 0]
+                    "scatter_conv_single", precision)[0, 0]
     if counter is not None:
         counter.add(x.shape[0] * x.shape[1] * k.shape[0] * k.shape[1],
                     clipped_writes(x.shape[0], x.shape[1], k.shape[0], k.shape[1]))
@@ -356,8 +378,12 @@ def scatter_conv_single(x: torch.Tensor, k: torch.Tensor, counter: MultCounter |
 
 def tiled_scatter_conv(x: torch.Tensor, w: torch.Tensor, cfg: TileConfig, workers: int,
                        counter: MultCounter | None = None, aux: AuxMemCounter | None = None,
-                       strategy: ScatterStrategy = ScatterStrategy.tile_private):
-    """scatter_conv.hpp:330-368 -- the shipped drop-in entry point (R = 1)."""
+                       strategy: ScatterStrategy = ScatterStrategy.tile_private, *,
+                       precision: str | None = None):
+    """scatter_conv.hpp:330-368 -- the shipped drop-in entry point (R = 1).
+
+    AuxMemCounter follows the reference's accounting (:351-360): tile_private acquires and
+    releases tile_h * tile_w * sizeof(float) * workers bytes; phase_parallel none."""
     cin = x.shape[-3]
     if cin != w.shape[1]:
         raise ValueError("tiled_scatter_conv: channel mismatch")
@@ -369,14 +395,14 @@ def tiled_scatter_conv(x: torch.Tensor, w: torch.Tensor, cfg: TileConfig, worker
         raise ValueError("tiled_scatter_conv: invalid halo")
     if workers < 1:
         raise ValueError("tiled_scatter_conv: workers must be >= 1")
-    desc, xb, squeeze = _single_desc(x, w, "scatter")
-    ws = desc.workspace_bytes()
+    desc, xb, squeeze = _single_desc(x, w, "scatter", precision)
+    aux_bytes = cfg.tile_h * cfg.tile_w * 4 * workers
     if aux is not None and strategy == ScatterStrategy.tile_private:
-        aux.acquire(ws)
+        aux.acquire(aux_bytes)
     bank = bank_precompute(desc, w)
     y, _ = ri_conv_forward(desc, xb, bank)
     if aux is not None and strategy == ScatterStrategy.tile_private:
-        aux.release(ws)
+        aux.release(aux_bytes)
     if counter is not None:
         counter.add(*desc.analytic_counts())
     y = y[:, :, 0]
@@ -427,9 +453,11 @@ def build_orientation_bank(basis: SteerableBasis, n: int):
 
 
 def group_conv_scatter_reuse(x: torch.Tensor, w: torch.Tensor, g: GroupSpec,
-                             counter: MultCounter | None = None) -> torch.Tensor:
+                             counter: MultCounter | None = None, *,
+                             precision: str | None = None) -> torch.Tensor:
     """SPEC:274-282 -> OrientedFeature (Cout, |G|, H, W) (batched: leading N)."""
-    y, _ = ri_conv(x, w, None, group=g.kind, orientations=g.size, pool="none", counter=counter)
+    y, _ = ri_conv(x, w, None, group=g.kind, orientations=g.size, pool="none", counter=counter,
+                   precision=precision or DEFAULT_PRECISION)
     return y
 
 

@@ -220,6 +220,12 @@ static void test_multi_and_tiled() {
     MultCounter mc;
     auto y = scatter_conv_multi(x, w, &mc);
     CHECK(std::memcmp(y.data(), ref.data(), ref.size() * 4) == 0, "scatter_conv_multi cin=%d k=%d", c.cin, c.k);
+    {  // the FP32 CUDA-core path, selected per thread, agrees bit-for-bit on dyadic inputs
+      b200::PrecisionScope fp32(b200::Precision::fp32);
+      auto y32 = scatter_conv_multi(x, w);
+      CHECK(std::memcmp(y32.data(), ref.data(), ref.size() * 4) == 0, "scatter_conv_multi fp32 cin=%d", c.cin);
+    }
+    CHECK(b200::precision() == b200::Precision::automatic, "default precision restored");
     auto yr = scatter_conv_raw_multi(x, w);
     CHECK(std::memcmp(yr.data(), rraw.data(), ref.size() * 4) == 0, "scatter_conv_raw_multi k=%d", c.k);
     CHECK(mc.scalar_multiplications == (unsigned long long)c.h * c.w * c.k * c.k * c.cin * c.cout, "multi mults");
@@ -233,6 +239,9 @@ static void test_multi_and_tiled() {
                   tc.scalar_additions == detail::clipped_writes(c.h, c.w, c.k, c.k) * c.cout,
               "tiled counters");
         CHECK(aux.current_bytes == 0, "aux released");
+        // the reference's accounting (scatter_conv.hpp:351-360): 5x5 float tiles x 4 workers
+        CHECK(aux.peak_bytes == (strat == ScatterStrategy::tile_private ? 5u * 5u * 4u * 4u : 0u),
+              "aux peak %zu", aux.peak_bytes);
       }
     }
   }

@@ -31,7 +31,7 @@ def test_library_exports_every_declared_symbol():
     for s in declared_symbols():
         assert hasattr(L, s), s
         assert s in _lib.SIGNATURES, f"{s} has no ctypes signature"
-    assert L.rc_abi_version() == 2
+    assert L.rc_abi_version() == 3
 
 
 def test_validation_messages_match_reference():
@@ -63,7 +63,7 @@ def test_tiled_host_entry_validates_like_reference():
              ((2, 4, 4, 3, 2, 3, 3, 32, 32, 1, 0), "tiled_scatter_conv: workers must be >= 1")]
     for (cin, h, w, cout, cinw, kh, kw, th, tw, halo, workers), msg in cases:
         st = L.rc_tiled_scatter_conv_host(z, cin, h, w, z, cout, cinw, kh, kw, th, tw, halo, workers,
-                                          0, z, None, None, None, 0)
+                                          0, z, None, None, None, 0, 0)
         assert st == _lib.RC_ERR_INVALID and _lib.last_error() == msg
 
 
@@ -88,9 +88,54 @@ def test_analytic_counts_and_shards():
 
 def test_kernel_selection():
     import paper_2512_08888_b200 as P
-    assert P.Desc(256, 256, 16, 16, 1024, 3, "steer", 8, "subgroup", 4).kernel_name().startswith("simt_k3")
-    assert P.Desc(32, 64, 8, 8, 256, 3).kernel_name().startswith("simt_k3")
+    c3 = dict(n=256, c_in=256, h=16, w=16, c_out=1024, k=3, group="steer", orientations=8,
+              pool="subgroup", pool_group=4)
+    assert P.Desc(**c3).precision == "auto"
+    assert P.Desc(**c3).kernel_name() == "tc_k3w16_bf16x3"
+    assert P.Desc(**c3, precision="fp32").kernel_name().startswith("simt_k3")
+    assert P.Desc(32, 64, 8, 8, 256, 3).kernel_name() == "tc_k3img8_bf16x3"
+    assert P.Desc(32, 64, 8, 8, 256, 3, precision="fp32").kernel_name().startswith("simt_k3")
     assert P.Desc(2, 3, 7, 5, 4, 5, "p4", 4, "max").kernel_name() == "generic"
+    assert P.Desc(8, 3, 64, 64, 64, 3, "steer", 8, "subgroup", 4).kernel_name().startswith("simt_k3")
+
+
+def test_dropin_entry_points_run_the_default_tensor_core_kernels():
+    """Every reference-named entry point defaults to precision auto; at the C1 (8x8x64->256,
+    R=1) and C3 (16x16x256->1024, steer R=8) shapes that is the tcgen05 kernel."""
+    import torch
+    import paper_2512_08888_b200 as P
+    from paper_2512_08888_b200 import _lib
+    x1, w1 = torch.empty(32, 64, 8, 8), torch.empty(256, 64, 3, 3)
+    for conv in ("scatter", "raw"):   # tiled_scatter_conv, scatter_conv_multi, scatter_conv_raw_multi
+        d, _, _ = P.rotconv._single_desc(x1, w1, conv)
+        assert d.kernel_name() == "tc_k3img8_bf16x3", (conv, d.kernel_name())
+    d, _, _ = P.rotconv._single_desc(x1, w1, "scatter", "fp32")
+    assert d.kernel_name().startswith("simt_k3")
+    # RIConv / ri_conv at C3
+    layer = P.RIConv(torch.empty(1024, 256, 3, 3), torch.empty(1024, 256, 3, 3))
+    assert layer.desc(256, 16, 16).kernel_name() == "tc_k3w16_bf16x3"
+    # the C-ABI host drop-in (rc_tiled_scatter_conv_host) builds precision AUTO (0) descs
+    cd = _lib.rc_desc(1, 64, 8, 8, 256, 3, 0, 1, 0, 1, 0, 0, 0)
+    assert _lib.lib().rc_kernel_name(C.byref(cd)) == b"tc_k3img8_bf16x3"
+    cd = _lib.rc_desc(256, 256, 16, 16, 1024, 3, 3, 8, 3, 4, 0, 0, 0)
+    assert _lib.lib().rc_kernel_name(C.byref(cd)) == b"tc_k3w16_bf16x3"
+
+
+def test_kernel_size_bound_is_validated():
+    """K > 11 is refused before any table sized for 11x11 taps is touched (all entry points
+    validate first); K = 11 is accepted by the generic kernel."""
+    import paper_2512_08888_b200 as P
+    from paper_2512_08888_b200 import _lib
+    for k, group in ((13, "single"), (13, "p4"), (15, "p4m")):
+        d = P.Desc(1, 2, 16, 16, 3, k, group, {"single": 1, "p4": 4, "p4m": 8}[group])
+        with pytest.raises(_lib.RotconvError, match="kernel size > 11 unsupported"):
+            d.validate()
+        assert d.bank_bytes() == 0 and d.workspace_bytes() == 0 and d.kernel_name() is None
+    assert P.Desc(1, 2, 16, 16, 3, 11, "p4", 4).kernel_name() == "generic"
+    z = C.c_void_p(0)
+    st = _lib.lib().rc_tiled_scatter_conv_host(z, 2, 16, 16, z, 3, 2, 13, 13, 32, 32, 6, 1, 0, z,
+                                               None, None, None, 0, 0)
+    assert st == _lib.RC_ERR_UNSUPPORTED and "kernel size > 11" in _lib.last_error()
 
 
 def test_product_never_imports_the_oracle():

@@ -1,4 +1,6 @@
-"""GPU parity: the sm_100a kernels vs the CPU oracle (which is pinned to the reference).
+"""GPU parity: the FP32 CUDA-core kernels (precision="fp32") vs the CPU oracle (which is
+pinned to the reference).  The shipped default (precision="auto", the tcgen05 kernels) is
+checked at full config sizes in test_gpu_shipped_default.py.
 
 Tolerances (FP32 path, stated here as the contract):
   * dyadic inputs (values k/4): bit-exact values AND argmax (every product and partial
@@ -21,10 +23,11 @@ pytestmark = pytest.mark.gpu
 NORMWISE_TOL = 2e-6
 
 
-def gpu_forward(P, d, x, w0, w1=None, bias=None, dev="cuda:0"):
+def gpu_forward(P, d, x, w0, w1=None, bias=None, dev="cuda:0", precision="fp32"):
     t = lambda a: None if a is None else torch.from_numpy(np.ascontiguousarray(a)).to(dev)
     desc = P.Desc(**{k: getattr(d, k) for k in ("n", "c_in", "h", "w", "c_out", "k", "group",
-                                                  "orientations", "pool", "pool_group", "convention")})
+                                                  "orientations", "pool", "pool_group", "convention")},
+                  precision=precision)
     bank = P.bank_precompute(desc, t(w0), t(w1))
     y, a = P.ri_conv_forward(desc, t(x), bank, t(bias))
     torch.cuda.synchronize()
@@ -161,11 +164,11 @@ def test_golden_fixtures_on_gpu(O, dev, golden):
         xt, wt = torch.from_numpy(x).to(dev), torch.from_numpy(w).to(dev)
         cnt = P.MultCounter()
         k = w.shape[2]
-        y = P.tiled_scatter_conv(xt, wt, P.TileConfig(32, 32, k // 2), 4, cnt).cpu().numpy()
+        y = P.tiled_scatter_conv(xt, wt, P.TileConfig(32, 32, k // 2), 4, cnt, precision="fp32").cpu().numpy()
         ref = golden[f"tiled_{i}_y"]
         assert np.abs(y - ref).max() <= NORMWISE_TOL * max(np.abs(ref).max(), 1e-30)
         assert [cnt.scalar_multiplications, cnt.scalar_additions] == list(golden[f"tiled_{i}_counts"])
-        yr = P.scatter_conv_raw_multi(xt, wt).cpu().numpy()
+        yr = P.scatter_conv_raw_multi(xt, wt, precision="fp32").cpu().numpy()
         refr = golden[f"raw_{i}_y"]
         assert np.abs(yr - refr).max() <= NORMWISE_TOL * max(np.abs(refr).max(), 1e-30)
     for i in range(5):
@@ -218,7 +221,7 @@ def test_tiled_scatter_conv_dropin_vs_reference(O, dev):
 
 
 def test_full_c3_subset_and_virtual_shards(O, dev):
-    """C3 at full size (N=256, 16x16x256->1024, steer R=8, subgroup-4): images 0 and 255
+    """FP32 CUDA-core kernel: C3 at full size (N=256, 16x16x256->1024, steer R=8, subgroup-4): images 0 and 255
     against the oracle; the whole batch equals the concatenation of two half-batch
     launches (virtual shards, bit-identical); run-to-run determinism."""
     import paper_2512_08888_b200 as P
@@ -229,12 +232,12 @@ def test_full_c3_subset_and_virtual_shards(O, dev):
     fx = (torch.rand((cout, cin, 3, 3), generator=g, device=dev) * 2 - 1) * s
     fy = (torch.rand((cout, cin, 3, 3), generator=g, device=dev) * 2 - 1) * s
     bias = (torch.rand(cout, generator=g, device=dev) * 0.2 - 0.1)
-    d = P.Desc(n, cin, h, w, cout, 3, "steer", 8, "subgroup", 4)
+    d = P.Desc(n, cin, h, w, cout, 3, "steer", 8, "subgroup", 4, "scatter", "fp32")
     bank = P.bank_precompute(d, fx, fy)
     y, a = P.ri_conv_forward(d, x, bank, bias)
     y2, a2 = P.ri_conv_forward(d, x, bank, bias)
     assert torch.equal(y, y2) and torch.equal(a, a2)
-    dh = P.Desc(n // 2, cin, h, w, cout, 3, "steer", 8, "subgroup", 4)
+    dh = P.Desc(n // 2, cin, h, w, cout, 3, "steer", 8, "subgroup", 4, "scatter", "fp32")
     yh0, ah0 = P.ri_conv_forward(dh, x[: n // 2].contiguous(), bank, bias)
     yh1, ah1 = P.ri_conv_forward(dh, x[n // 2:].contiguous(), bank, bias)
     assert torch.equal(torch.cat([yh0, yh1]), y) and torch.equal(torch.cat([ah0, ah1]), a)
