@@ -353,8 +353,6 @@ IgPlan ig_plan(const IgGeom& g, int parts) {
 }  // namespace
 
 bool igemm_supported(const rc_desc& d) {
-  const char* e = getenv("RC_TC_IGEMM");  // A/B switch (default on)
-  if (e && e[0] == '0') return false;
   // whole 8x8 / 4x4 images: the band kernels' small-image geometry has neither halo nor pad
   // (the padded grid here would be 1.56x / 2.25x the pixels); C1: 16.5 vs 31.5 us
   if ((d.w == 8 && d.h == 8) || (d.w == 4 && d.h == 4)) return false;
@@ -431,9 +429,7 @@ int launch_igemm(const rc_desc& d, const float* x, const uint8_t* wpk, const uin
   p.w_stages = plan.w_stages;
   p.act = d.activation;
   {
-    const char* se = getenv("RC_IGEMM_SEG");  // A/B: chunks per accumulation segment
-    p.seg = se ? atoi(se) : 8;
-    if (p.seg < 1) p.seg = 1;
+    p.seg = 8;  // chunks per accumulation segment (profiles/r01/igemm/acc_probe.txt)
   }
   TapOffsets to;
   slice_tap_offsets(3, d.convention, &to);

@@ -424,8 +424,7 @@ int launch_simt_k3(const rc_desc& d, const float* x, const void* bank, const flo
   int SW, S;
   // SW columns per thread: 8 keeps more work per thread, 4 halves the register state
   // (3-row x 4-rotation accumulators) so more warps fit per SM; RC_SIMT_SW selects (A/B)
-  const char* swe = getenv("RC_SIMT_SW");
-  const int sw_pref = swe ? atoi(swe) : 8;
+  const int sw_pref = 8;  // 8-column segments for 8-wide images (profiles/r01/simt_sw_ab.txt)
   switch (d.w) {
     case 4: SW = 4; S = 1; break;
     case 8: SW = sw_pref == 4 ? 4 : 8; S = 8 / SW; break;
@@ -471,8 +470,7 @@ int launch_simt_k3(const rc_desc& d, const float* x, const void* bank, const flo
   p.act = d.activation;
   size_t smem = 2 * sizeof(float) * ((size_t)IMG * CC * d.w + (size_t)CC * COB * 12);
   const size_t smem_res = sizeof(float) * ((size_t)IMG * d.c_in * d.h * d.w + (size_t)p.NB * d.c_in * COB * 12);
-  const char* re = getenv("RC_SIMT_RESIDENT");  // A/B switch (default on)
-  p.resident = (re ? atoi(re) : 1) && d.c_in <= CC && smem_res <= 200 * 1024;
+  p.resident = d.c_in <= CC && smem_res <= 200 * 1024;
   if (p.resident) smem = std::max(smem, smem_res);
   const int gx = (d.c_out + COB - 1) / COB, gy = (d.n + IMG - 1) / IMG;
   if (gy > 65535) return RC_ERR_UNSUPPORTED;

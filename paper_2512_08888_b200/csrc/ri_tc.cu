@@ -1,24 +1,34 @@
-// ri_tc.cu -- tcgen05 tensor-core fused RI scatter convolution, K = 3, W = 16 (sm_100a).
+// ri_tc.cu -- tcgen05 tensor-core fused RI scatter convolution, K = 3 (sm_100a).
 //
 // Same math as ri_simt.cu (convention P1), with the channel contraction on
 // the 5th-generation tensor cores:
 //   Z_t[co, px] = sum_ci W_{b,t}[co, ci] * X[ci, px]      tcgen05.mma kind::f16, M = 128 co,
-//                                                         N = 96 px, FP32 accumulators in TMEM
+//                                                         N = band px, FP32 accumulators in TMEM
 //   Y_{b,r}(p) += Z_t(p + delta_{r,t})                    CUDA-core epilogue, reused by all 4 r
 // precision "bf16"  : one product, bf16 operands;
 // precision "bf16x3": operands split hi + lo (bf16 each); hi*hi + hi*lo + lo*hi, FP32-class.
 //
-// Work item = (co tile of 128, image); per base b the image is swept in bands of 4 output
-// rows.  A band's MMA covers the 6 input rows [4k-1, 4k+5) (one halo row above and below,
-// recomputed: 1.5x the MMA work, no cross-band state in TMEM and no cross-warp races).
+// Work item = (co tile of 128, image); per base b the image is swept in bands of 64 output
+// pixels.  A 16-wide band is 4 output rows computed from the 6 input rows [4k-1, 4k+5) (the
+// halo rows are recomputed: no cross-band state in TMEM and no cross-warp races); bands at
+// the image top / bottom skip the halo rows outside the image.
 //
 // Persistent CTA (1 per SM), 20 warps:
-//   warp 0      producer  : 1-D bulk copies (TMA engine) of pre-packed SW128 tiles: the X
-//                           band (NC tiles of [96 px x 64 ci]) and, per stage, spc ci-chunks of
-//                           one tap's weights [128 co x 64 ci] (>= 32 KB per copy).
-//   warp 1      MMA       : elected lane issues tcgen05.mma (M=128, N=96, K=16) into one of
-//                           NDB TMEM buffers per (base, band, tap) and commits to mbarriers.
-//   warps 2, 3  idle (complete the producer warpgroup for setmaxnreg).
+//   warps 1, 2  MMA       : two issuers, alternating taps (warp 1 the even, warp 2 the odd taps
+//                           of the global tap sequence).  An elected lane issues tcgen05.mma
+//                           (M = 128, K = 16) into the tap's TMEM buffer and commits to
+//                           mbarriers.  The tensor pipe's issue queue is shallow, so every
+//                           barrier wait / commit / fence of a single issuer is a pipe bubble;
+//                           with two issuers one warp's synchronisation overlaps the other's
+//                           MMAs (tools/mma_sync_probe.cu: 67.9 -> 56.1 cycles per N = 96 MMA,
+//                           the shared-memory operand floor; profiles/r02/probe/).
+//   warps 0, 3  producers : 1-D bulk copies (TMA engine) of pre-packed SW128 tiles, one
+//                           producer per MMA warp, each filling that warp's own W ring (stages
+//                           of spc ci-chunks of one tap's weights [128 co x 64 ci], hi + lo).
+//                           Private rings are consumed strictly in order, so no waiter can
+//                           reach for a slot's next mbarrier phase before the current one has
+//                           completed (the parity of phase n+1 is that of phase n-1).  Warp 0
+//                           also loads the X band (NC tiles of [MMA_N px x 64 ci]).
 //   warps 4-19  epilogue  : TMEM lane = output channel co.  The 4 warps of a lane quadrant
 //                           own the band's 4 output rows (one each); a thread holds
 //                           Y[4 rotations][16 px] = 64 fp32 registers, pulls the 3 input rows
@@ -41,62 +51,39 @@ using namespace tc;
 // Band geometry.  A band is 64 output pixels (the register budget of the epilogue: every
 // epilogue thread owns 16 of them) computed from the input rows/columns they depend on:
 //   TW = 16 : 4 full rows of a 16-wide image from 6 input rows           (N = 96)
-//   TW = 32 : 2 full rows of a 32-wide image from 4 input rows           (N = 128)
-//   TW = 0  : strip of 4 rows x 16 columns of a wider image (W % 16 == 0, W >= 48) from
+//   TW = 0  : strip of 4 rows x 16 columns of a wider image (W % 16 == 0, W >= 32) from
 //             6 input rows x 18 columns incl. the halo columns           (N = 112, 108 used)
-// RS is the TMEM / operand row stride (pixels per input row of the band).
 //   TW = 8, 4 (H == W): small images, whole images per band and no halo rows at all (the
 //             window rows outside an image are the zero padding): 1 image of 8x8 or 4
 //             images of 4x4 per band (N = 64); a thread owns TR = 16/W full rows.
-// Experiment (off): bf16x3 with the hi weight tile (read by 2 of the 3 products) copied to
-// TMEM once per chunk with tcgen05.cp and consumed by TS MMAs, so shared memory serves Ah
-// once instead of twice.  Bit-identical, but 15% slower on C3 and C4
-// (profiles/r01/tsa_ab.txt): the copy -> MMA dependency costs more than the saved reads.
-#ifndef RC_TC_TSA
-#define RC_TC_TSA 0
-#endif
-constexpr bool kTsa = RC_TC_TSA != 0;
-// Experiment: bf16x3 for 16-wide images as 2 MMAs per K-step: Wh x [Xh; Xl] (N = 192, D
-// columns 0-95 = Wh Xh, 96-191 = Wh Xl) and Wl x Xh (N = 96, into columns 0-95); the
-// epilogue adds the two halves.  A third fewer MMA instructions, a third fewer weight reads.
-#ifndef RC_TC_CONCAT
-#define RC_TC_CONCAT 0
-#endif
-constexpr bool kConcat = RC_TC_CONCAT != 0;
-#ifndef RC_TC_ROWBYROW
-#define RC_TC_ROWBYROW 1
-#endif
-constexpr bool kRowByRow = RC_TC_ROWBYROW != 0;  // epilogue loads one window row at a time
-constexpr uint32_t A_COL0 = 448;  // TMEM columns [448, 512): two Ah regions
-
+// RS is the TMEM / operand row stride (pixels per input row of the band).
+// (Measured and rejected in round 1, not shipped: 2-row bands for W = 32, CTA pairs, the hi
+// weight tile staged in TMEM, N = 192 hi/lo concatenation -- DESIGN.md 3.1.)
 template <int TW>
 struct Geo {
   static constexpr bool STRIP = TW == 0;
   static constexpr bool SMALL = TW == 4 || TW == 8;
-  static constexpr int OUT_ROWS = STRIP ? 4 : (SMALL ? 64 / TW : 64 / TW);  // 4 | 2 | 4 | 8 | 16
+  static constexpr int OUT_ROWS = STRIP ? 4 : 64 / TW;        // 4 | 4 | 8 | 16
   static constexpr int IN_ROWS = SMALL ? OUT_ROWS : OUT_ROWS + 2;
   static constexpr int RS = STRIP ? 18 : TW;                  // pixels per band row
-  static constexpr int BAND_PX = IN_ROWS * RS;                // 96 | 128 | 108 | 64 | 64
+  static constexpr int BAND_PX = IN_ROWS * RS;                // 96 | 108 | 64 | 64
   static constexpr int MMA_N = (BAND_PX + 15) / 16 * 16;
   static constexpr int XTILE = MMA_N * 64 * 2;                // bytes of one [MMA_N x 64 ci] bf16 tile
-  static constexpr int HALVES = (STRIP || SMALL) ? 1 : TW / 16;  // epilogue threads per output row
   // D buffers from column D0.  Columns [0, D0) keep the 1-column-left halo load of a band's
   // first pixel inside the allocation; full-row bands also read their skipped (out-of-image)
   // window rows from them as zeros (band_rows), so they need D0 >= 18.
-  static constexpr bool CAT = kConcat && TW == 16;          // D buffer = [hi 96 | lo 96]
-  static constexpr uint32_t D0 = CAT ? 0 : ((STRIP || SMALL) ? 16 : 32);
-  // bf16x3 with Ah staged in TMEM (kTsa) keeps 2 x 32 columns at the top for it
-  static constexpr uint32_t TOP = kTsa ? 64 : 0;
-  static constexpr int DCOLS = CAT ? 2 * MMA_N : MMA_N;     // TMEM columns per D buffer
-  static constexpr int NDB = DCOLS * 5 + D0 + TOP <= 512 ? 5
-                             : (DCOLS * 4 + D0 + TOP <= 512 ? 4 : (DCOLS * 3 + D0 + TOP <= 512 ? 3 : 2));
+  static constexpr uint32_t D0 = (STRIP || SMALL) ? 16 : 32;
+  static constexpr int DCOLS = MMA_N;                         // TMEM columns per D buffer
+  static constexpr int NDB = DCOLS * 5 + D0 <= 512 ? 5 : (DCOLS * 4 + D0 <= 512 ? 4 : 3);
   static constexpr int TR = SMALL ? 16 / TW : 1;              // output rows per epilogue thread
   static constexpr int IMGS = SMALL ? 64 / (TW * TW) : 1;     // images per band
+  static constexpr bool TRIM = !STRIP && !SMALL;              // full-row bands: see band_rows
 };
 constexpr int KC = 64;                  // ci per chunk (one 128-byte swizzle row of bf16)
 constexpr int WTILE = 128 * KC * 2;      // 16 KB
 constexpr int NUM_EPI = 16;              // epilogue warps (4 warpgroups)
-constexpr int EPI_WARP0 = 4;             // warps 0-3: producer warpgroup (TMA, MMA, 2 idle)
+constexpr int EPI_WARP0 = 4;             // warps 0-3: producer warpgroup (TMA, 2 x MMA, idle)
+constexpr int NUM_MMA = 2;               // MMA-issuing warps (1 and 2)
 constexpr int THREADS = 32 * (EPI_WARP0 + NUM_EPI);
 constexpr int REGS_PRODUCER = 64;        // setmaxnreg budgets: 20 warps x 96 at launch; the MMA
                                          // warp's loop spills at 32 (-2..5% with 64/104,
@@ -104,6 +91,7 @@ constexpr int REGS_PRODUCER = 64;        // setmaxnreg budgets: 20 warps x 96 at
 constexpr int REGS_EPILOGUE = 104;
 constexpr int MAX_NDB = 5;
 constexpr int MAX_NC = 8;                // ci chunks of 64 (Cin <= 512)
+constexpr int MAX_STAGES = 8;
 constexpr int XH = 16;                   // output columns per epilogue thread
 
 // Input rows [first, end) of full-row band k (band rows 0 .. IN_ROWS-1 = image rows
@@ -115,7 +103,7 @@ __device__ __forceinline__ int2 band_rows(int k, int H) {
 }
 
 struct TcParams {
-  const uint8_t* xh;  // packed X tiles [n][band][chunk] (hi), 12 KB each
+  const uint8_t* xh;  // packed X tiles [n][band][chunk] (hi), XTILE bytes each
   const uint8_t* xl;  // lo plane (3-pass) or null
   const uint8_t* w;   // packed W tiles: bf16x3 [b][ct][t][chunk][part], bf16 [b][ct][t][chunk]
   const float* bias;
@@ -125,10 +113,6 @@ struct TcParams {
   int xstream;  // 1: X chunks travel with the W stages (the X band does not fit in smem)
   float inv_r;  // 1/R for average pooling (R a power of two)
   int act;      // rc_activation applied after the bias (last op of the epilogue)
-  int ablate;   // profiling only: 1 = skip stores, 2 = skip MMAs, 3 = skip MMAs + W loads,
-                // 4 = skip W loads (MMAs on stale tiles), 5 = epilogue skips TMEM loads + scatter,
-                // 6 = 4 + 5 (the bare MMA issue stream)
-  int trim;     // full-row bands skip their out-of-image halo rows (band_rows); 0 = A/B switch
 };
 
 // ---- TMEM -> registers ----------------------------------------------------------------
@@ -250,7 +234,7 @@ __device__ __forceinline__ void finalize_row(const TcParams& p, float (&Yr)[RPB]
 // ---- scatter ------------------------------------------------------------------------
 // A thread's 16 output columns [x0, x0+16) of output row o read input rows o-1 .. o+1
 // (D-buffer rows s .. s+2).  z[c] holds input column x0 - 1 + c (c = 0..17); columns
-// outside the image were loaded as 0 (TW = 32) or are skipped at compile time (TW = 16:
+// outside the image are zero in the band (strips) or are skipped at compile time (TW = 16:
 // the thread's 16 columns are the whole row).  Y_r(p) += Z_t(p + (di, dj)): for tap T and
 // rotation r the single contributing row is I = 1 + di.
 template <int TW, int RPB, int CONV, int T, int I>
@@ -276,13 +260,8 @@ __device__ __forceinline__ void tmem_zero32(uint32_t taddr) {  // columns [0, 32
                  : "memory");
   asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
 }
-__device__ __forceinline__ float tmem_ld1(uint32_t taddr) {
-  uint32_t r;
-  asm volatile("tcgen05.ld.sync.aligned.32x32b.x1.b32 {%0}, [%1];\n" : "=r"(r) : "r"(taddr));
-  return __uint_as_float(r);
-}
 
-// one input row of the thread's window: 16 columns + (TW = 32) the two halo columns
+// one input row of a strip thread's window: the two halo columns after its 16
 __device__ __forceinline__ void tmem_ld2f(uint32_t taddr, float& a, float& b) {
   uint32_t r0, r1;
   asm volatile("tcgen05.ld.sync.aligned.32x32b.x2.b32 {%0,%1}, [%2];\n" : "=r"(r0), "=r"(r1) : "r"(taddr));
@@ -290,21 +269,8 @@ __device__ __forceinline__ void tmem_ld2f(uint32_t taddr, float& a, float& b) {
   b = __uint_as_float(r1);
 }
 
-// two consecutive 16-column band rows (TW = 16) in one x32 load: z[1..16], z1[1..16]
-__device__ __forceinline__ void tmem_ld_rows2(uint32_t taddr, float (&z)[18], float (&z1)[18]) {
-  uint32_t r[32];
-  asm volatile("tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];\n"
-               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
-               : "r"(taddr));
-#pragma unroll
-  for (int i = 0; i < 16; ++i) {
-    z[1 + i] = __uint_as_float(r[i]);
-    z1[1 + i] = __uint_as_float(r[16 + i]);
-  }
-}
-
-// one input row of the thread's window: 16 columns + (TW = 32, strips) the halo columns.
-// issue_row only issues the TMEM loads; finish_row (after tcgen05.wait::ld) fixes edges.
+// one input row of the thread's window: 16 columns + (strips) the halo columns.
+// issue_row only issues the TMEM loads; the caller waits (tcgen05.wait::ld).
 template <int TW>
 __device__ __forceinline__ void issue_row(uint32_t a, float (&z)[18]) {
   if constexpr (TW == 0) {  // strip: the band row holds the halo columns (zero at image edges)
@@ -312,24 +278,12 @@ __device__ __forceinline__ void issue_row(uint32_t a, float (&z)[18]) {
     tmem_ld2f(a + 16, z[16], z[17]);
   } else {
     tmem_ld16(a, *reinterpret_cast<float(*)[16]>(&z[1]));
-    if (TW == 32) {
-      z[0] = tmem_ld1(a - 1);
-      z[17] = tmem_ld1(a + 16);
-    }
   }
 }
 template <int TW>
-__device__ __forceinline__ void finish_row(int half, float (&z)[18]) {
-  if (TW == 32) {  // image edges: the neighbouring half does not exist
-    if (half == 0) z[0] = 0.f;
-    if (half == TW / 16 - 1) z[17] = 0.f;
-  }
-}
-template <int TW>
-__device__ __forceinline__ void load_row(uint32_t a, int half, float (&z)[18]) {
+__device__ __forceinline__ void load_row(uint32_t a, float (&z)[18]) {
   issue_row<TW>(a, z);
   tmem_wait_ld();
-  finish_row<TW>(half, z);
 }
 
 // small images: window row I (input row o0 - 1 + I) feeds output row i of the thread's TR
@@ -377,40 +331,33 @@ __device__ __forceinline__ void small_row(uint32_t a, int o0, float (&Y)[RPB][XH
   scatter_small<TW, RPB, CONV, T, I>(Y, z);
 }
 
-// concatenated bf16x3 (Geo::CAT): window row I = hi half + lo half of the D buffer
-template <int TW, int RPB, int CONV, int T, int I>
-__device__ __forceinline__ void cat_row(uint32_t a, float (&Y)[RPB][XH]) {
-  float z[18], t[16];
-  tmem_ld16(a + I * 16, *reinterpret_cast<float(*)[16]>(&z[1]));
-  tmem_ld16(a + Geo<TW>::MMA_N + I * 16, t);
-  tmem_wait_ld();
-#pragma unroll
-  for (int j = 0; j < 16; ++j) z[1 + j] += t[j];
-  scatter_row<TW, RPB, CONV, T, I>(Y, z);
-}
-
 struct EpiState {
   uint32_t row_base;  // TMEM address of D-buffer 0, first input row of the thread, its columns
   int db;
   uint32_t dph;
-  int lane, half;
-  uint32_t dempty_cl;  // CTA pairs: shared::cluster address of the leader's d_empty[0]
+  int lane;
   int o0;              // small images: first output row of the thread (within its image)
   int vmask;           // window rows 0..2 inside the image (bit I); the others were not computed
   uint32_t zero_addr;  // TMEM columns [0, D0) of the thread's lane: zeros (full-row bands)
-  int cat;             // concatenated bf16x3 D buffers (Geo::CAT, resident X)
 };
 
+__device__ __forceinline__ void release_d(EpiState& e, int ndb, uint64_t* d_empty) {
+  tc_fence_before();
+  __syncwarp();
+  if (e.lane == 0) mbar_arrive(&d_empty[e.db]);  // D buffer free: an MMA warp may refill it
+  if (++e.db == ndb) {
+    e.db = 0;
+    e.dph ^= 1;
+  }
+}
+
 // one tap (compile-time T): three single-row TMEM round trips, D released after the last
-template <int TW, int RPB, int CONV, int T, bool PAIR>
+template <int TW, int RPB, int CONV, int T>
 __device__ __forceinline__ void epi_tap(EpiState& e, float (&Y)[RPB][XH], uint64_t* d_full, uint64_t* d_empty) {
   constexpr int NDB = Geo<TW>::NDB;
   const uint32_t a = e.row_base + e.db * Geo<TW>::DCOLS;
   float z[18];
-  if constexpr (PAIR)
-    mbar_wait_spin(&d_full[e.db], e.dph);  // pairs: arrived by the leader's multicast commit
-  else
-    mbar_wait(&d_full[e.db], e.dph);
+  mbar_wait(&d_full[e.db], e.dph);
   tc_fence_after();
   if constexpr (Geo<TW>::SMALL) {
     constexpr int TR = Geo<TW>::TR;
@@ -420,164 +367,80 @@ __device__ __forceinline__ void epi_tap(EpiState& e, float (&Y)[RPB][XH], uint64
     if constexpr (TR >= 2) small_row<TW, RPB, CONV, T, 3>(a, e.o0, Y);
     if constexpr (TR >= 4) small_row<TW, RPB, CONV, T, 4>(a, e.o0, Y);
     if constexpr (TR >= 4) small_row<TW, RPB, CONV, T, 5>(a, e.o0, Y);
-    tc_fence_before();
-    __syncwarp();
-    if (e.lane == 0) {
-      if constexpr (PAIR)
-        mbar_arrive_cluster(e.dempty_cl + e.db * 8);
-      else
-        mbar_arrive(&d_empty[e.db]);
-    }
-    if (++e.db == NDB) {
-      e.db = 0;
-      e.dph ^= 1;
-    }
+    release_d(e, NDB, d_empty);
     return;
   }
-  // window rows outside the image were not computed (band_rows): read the zero columns
-  if constexpr (Geo<TW>::CAT) {
-    if (e.cat) {  // D = [Wh Xh + Wl Xh | Wh Xl]: each window row is the sum of both halves
-      cat_row<TW, RPB, CONV, T, 0>(a, Y);
-      cat_row<TW, RPB, CONV, T, 1>(a, Y);
-      float z[18], t[16];
-      tmem_ld16(a + 2 * 16, *reinterpret_cast<float(*)[16]>(&z[1]));
-      tmem_ld16(a + Geo<TW>::MMA_N + 2 * 16, t);
-      tmem_wait_ld();
-      tc_fence_before();
-      __syncwarp();
-      if (e.lane == 0) mbar_arrive(&d_empty[e.db]);
-      if (++e.db == NDB) {
-        e.db = 0;
-        e.dph ^= 1;
-      }
-#pragma unroll
-      for (int j = 0; j < 16; ++j) z[1 + j] += t[j];
-      scatter_row<TW, RPB, CONV, T, 2>(Y, z);
-      return;
-    }
-  }
-  const int m = e.vmask;
-  if constexpr (kRowByRow && TW == 16) {
+  const int m = e.vmask;  // window rows outside the image were not computed: read zeros
+  if constexpr (TW == 16) {
     // one window row at a time: a TMEM round trip is ~22 cycles, and a single 16-value row
     // in flight keeps the epilogue's registers (Y = 64) clear of spills, which would share
     // the L1/shared-memory bandwidth the SS MMAs are bound by
-    load_row<TW>((m & 1) ? a : e.zero_addr, e.half, z);
+    load_row<TW>((m & 1) ? a : e.zero_addr, z);
     scatter_row<TW, RPB, CONV, T, 0>(Y, z);
-    load_row<TW>((m & 2) ? a + Geo<TW>::RS : e.zero_addr, e.half, z);
+    load_row<TW>((m & 2) ? a + Geo<TW>::RS : e.zero_addr, z);
     scatter_row<TW, RPB, CONV, T, 1>(Y, z);
-  } else {  // rows 0 and 1 in flight together: one TMEM round trip instead of two
+  } else {  // strips: rows 0 and 1 in flight together
     float z1[18];
-    if (TW == 16 && (m & 3) == 3) {
-      tmem_ld_rows2(a, z, z1);
-    } else {
-      issue_row<TW>((m & 1) ? a : e.zero_addr, z);
-      issue_row<TW>((m & 2) ? a + Geo<TW>::RS : e.zero_addr, z1);
-    }
+    issue_row<TW>(a, z);
+    issue_row<TW>(a + Geo<TW>::RS, z1);
     tmem_wait_ld();
-    finish_row<TW>(e.half, z);
-    finish_row<TW>(e.half, z1);
     scatter_row<TW, RPB, CONV, T, 0>(Y, z);
     scatter_row<TW, RPB, CONV, T, 1>(Y, z1);
   }
-  load_row<TW>((m & 4) ? a + 2 * Geo<TW>::RS : e.zero_addr, e.half, z);
-  tc_fence_before();
-  __syncwarp();
-  if (e.lane == 0) {  // D buffer free: the MMA may refill it (pairs: the leader's barrier)
-    if constexpr (PAIR)
-      mbar_arrive_cluster(e.dempty_cl + e.db * 8);
-    else
-      mbar_arrive(&d_empty[e.db]);
-  }
-  if (++e.db == NDB) {
-    e.db = 0;
-    e.dph ^= 1;
-  }
+  load_row<TW>((m & 4) ? a + 2 * Geo<TW>::RS : e.zero_addr, z);
+  release_d(e, NDB, d_empty);
   scatter_row<TW, RPB, CONV, T, 2>(Y, z);
 }
 
-// Epilogue warp: lane quadrant q (co = q*32 + lane); sub-tile sub = (output row of the
-// band, column half): TW = 16 -> 4 rows x 1 half, TW = 32 -> 2 rows x 2 halves.
-// Work schedule: item -> (image n, co tile ct).  Single CTAs walk items n*NCT + ct; CTA
-// pairs walk pair items n*(NCT/2) + ctp and CTA rank r of the pair takes ct = 2*ctp + r.
-struct Work {
-  int first, stride, count, per_n, rank;
-  __device__ __forceinline__ int n(int item) const { return item / per_n; }
-  __device__ __forceinline__ int ct(int item) const { return rank < 0 ? item % per_n : 2 * (item % per_n) + rank; }
-};
-template <bool PAIR>
-__device__ __forceinline__ Work make_work(const TcParams& p) {
-  if constexpr (PAIR)
-    return Work{(int)cluster_id_x(), (int)ncluster_x(), p.N * (p.NCT / 2), p.NCT / 2, (int)cluster_ctarank()};
-  else
-    return Work{(int)blockIdx.x, (int)gridDim.x, p.items, p.NCT, -1};
-}
-
-template <int TW, int RPB, int CONV, bool PAIR>
+// Epilogue warp: lane quadrant q (co = q*32 + lane); sub-tile sub = output row of the band.
+// Work schedule: CTA i walks items i, i + grid, ...; item -> (image n, co tile ct) =
+// (item / NCT, item % NCT).
+template <int TW, int RPB, int CONV>
 __device__ void epilogue(const TcParams& p, uint32_t tmem, uint64_t* d_full, uint64_t* d_empty) {
   using G = Geo<TW>;
-  constexpr bool TRIM = !G::STRIP && !G::SMALL && !PAIR && !G::CAT;  // see band_rows
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int q = warp % 4;
   const int sub = (warp - EPI_WARP0) / 4;
-  const int srow = sub / G::HALVES, half = sub % G::HALVES;
+  const int srow = sub;
   const int co_l = q * 32 + lane;
   // small images: sub = image of the band (4x4) or row pair (8x8); row_base -> its first row
   const int s_img = G::SMALL ? (G::IMGS > 1 ? sub : 0) : 0;
   const int o0 = G::SMALL ? (G::IMGS > 1 ? 0 : sub * G::TR) : 0;
-  const uint32_t rb = G::SMALL ? (uint32_t)((s_img * TW + o0) * G::RS) : (uint32_t)(srow * G::RS + half * 16);
-  EpiState e{tmem + ((uint32_t)(q * 32) << 16) + G::D0 + rb, 0, 0, lane, half,
-             PAIR ? mapa_shared(d_empty, 0) : 0u, o0, 7, tmem + ((uint32_t)(q * 32) << 16) + 1,
-             (G::CAT && !PAIR && p.passes == 3 && !p.xstream) ? 1 : 0};
-  if constexpr (TRIM) tmem_zero32(tmem + ((uint32_t)(q * 32) << 16));  // every warp of the quadrant
-                                                                        // writes the same zeros
+  const uint32_t rb = G::SMALL ? (uint32_t)((s_img * TW + o0) * G::RS) : (uint32_t)(srow * G::RS);
+  EpiState e{tmem + ((uint32_t)(q * 32) << 16) + G::D0 + rb, 0, 0, lane, o0, 7,
+             tmem + ((uint32_t)(q * 32) << 16) + 1};
+  if constexpr (G::TRIM) tmem_zero32(tmem + ((uint32_t)(q * 32) << 16));  // every warp of the quadrant
+                                                                           // writes the same zeros
   const int nstrip = G::STRIP ? p.W / 16 : 1;
   float Y[RPB][XH];
-  const Work wk = make_work<PAIR>(p);
-  for (int item = wk.first; item < wk.count; item += wk.stride) {
-    const int n = wk.n(item), ct = wk.ct(item);
+  for (int item = blockIdx.x; item < p.items; item += gridDim.x) {
+    const int n = item / p.NCT, ct = item % p.NCT;
     const int co = ct * 128 + co_l;
-    if (p.ablate == 5 || p.ablate == 6) {  // profiling: consume D buffers without reading them
-      for (int i = 0; i < p.NB * p.NBK * 9; ++i) {
-        mbar_wait(&d_full[e.db], e.dph);
-        __syncwarp();
-        if (lane == 0) {
-          if constexpr (PAIR)
-            mbar_arrive_cluster(e.dempty_cl + e.db * 8);
-          else
-            mbar_arrive(&d_empty[e.db]);
-        }
-        if (++e.db == G::NDB) {
-          e.db = 0;
-          e.dph ^= 1;
-        }
-      }
-      continue;
-    }
     for (int k = 0; k < p.NBK; ++k)
       for (int b = 0; b < p.NB; ++b) {
 #pragma unroll
         for (int r = 0; r < RPB; ++r)
 #pragma unroll
           for (int x = 0; x < XH; ++x) Y[r][x] = 0.f;
-        if (TRIM && p.trim) {
+        if constexpr (G::TRIM) {
           const int2 v = band_rows<TW>(k, p.H);
           e.vmask = 0;
 #pragma unroll
           for (int i = 0; i < 3; ++i) e.vmask |= (srow + i >= v.x && srow + i < v.y) ? 1 << i : 0;
         }
-        epi_tap<TW, RPB, CONV, 0, PAIR>(e, Y, d_full, d_empty);
-        epi_tap<TW, RPB, CONV, 1, PAIR>(e, Y, d_full, d_empty);
-        epi_tap<TW, RPB, CONV, 2, PAIR>(e, Y, d_full, d_empty);
-        epi_tap<TW, RPB, CONV, 3, PAIR>(e, Y, d_full, d_empty);
-        epi_tap<TW, RPB, CONV, 4, PAIR>(e, Y, d_full, d_empty);
-        epi_tap<TW, RPB, CONV, 5, PAIR>(e, Y, d_full, d_empty);
-        epi_tap<TW, RPB, CONV, 6, PAIR>(e, Y, d_full, d_empty);
-        epi_tap<TW, RPB, CONV, 7, PAIR>(e, Y, d_full, d_empty);
-        epi_tap<TW, RPB, CONV, 8, PAIR>(e, Y, d_full, d_empty);
+        epi_tap<TW, RPB, CONV, 0>(e, Y, d_full, d_empty);
+        epi_tap<TW, RPB, CONV, 1>(e, Y, d_full, d_empty);
+        epi_tap<TW, RPB, CONV, 2>(e, Y, d_full, d_empty);
+        epi_tap<TW, RPB, CONV, 3>(e, Y, d_full, d_empty);
+        epi_tap<TW, RPB, CONV, 4>(e, Y, d_full, d_empty);
+        epi_tap<TW, RPB, CONV, 5>(e, Y, d_full, d_empty);
+        epi_tap<TW, RPB, CONV, 6>(e, Y, d_full, d_empty);
+        epi_tap<TW, RPB, CONV, 7>(e, Y, d_full, d_empty);
+        epi_tap<TW, RPB, CONV, 8>(e, Y, d_full, d_empty);
         const int row = G::SMALL ? o0 : G::OUT_ROWS * (k / nstrip) + srow;
-        const int x0 = G::SMALL ? 0 : (k % nstrip) * 16 + half * 16;
+        const int x0 = G::SMALL ? 0 : (k % nstrip) * 16;
         const int img = G::SMALL ? n * G::IMGS + s_img : n;  // small: n indexes bands of IMGS images
-        if (img < p.N && co < p.Cout && row < p.H && p.ablate != 1) finalize_row<TW, RPB>(p, Y, img, co, b, row, x0);
+        if (img < p.N && co < p.Cout && row < p.H) finalize_row<TW, RPB>(p, Y, img, co, b, row, x0);
       }
   }
 }
@@ -595,60 +458,43 @@ struct Ring {
   }
 };
 
-// PAIR: a cluster of 2 CTAs issues M = 256 MMAs (tcgen05 cta_group::2) -- each CTA
-// supplies the weights of its own 128 output channels and HALF of the X band, so the
-// shared-memory operand traffic per MMA drops from 4 KB + N*32 B to 4 KB + N*16 B and the
-// N = 96 band MMA becomes math-bound.  The leader (rank 0) issues the MMAs; the peer's MMA
-// warp forwards "stage loaded" events to the leader; commits multicast to both CTAs; both
-// epilogues release D buffers on the leader's barrier.
-template <int TW, int RPB, int CONV, bool PAIR>
+template <int TW, int RPB, int CONV>
 __global__ void __launch_bounds__(THREADS, 1) ri_tc_kernel(const __grid_constant__ TcParams p) {
   using G = Geo<TW>;
-  constexpr bool TRIM = !G::STRIP && !G::SMALL && !PAIR && !G::CAT;  // see band_rows
   constexpr int NDB = G::NDB;
-  constexpr int XTILE = G::XTILE;                     // bytes of a full band tile (global layout)
-  constexpr int XS = PAIR ? XTILE / 2 : XTILE;        // bytes of this CTA's part of it in smem
+  constexpr int XS = G::XTILE;                        // bytes of a band tile
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   // 1 KB alignment for the SW128 atoms
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const int parts = p.passes == 3 ? 2 : 1;
   uint8_t* xs = smem;                           // X band: [part][chunk] tiles of XS bytes
   uint8_t* ws = smem + (p.xstream ? 0 : parts * p.NC * XS);  // W (+ X when streamed) ring
-  // per-chunk X barriers: chunk c of band k+1 is reloaded as soon as the MMAs of band k's
-  // last tap on chunk c complete, so band transitions overlap the last tap's MMAs
-  __shared__ uint64_t w_full[8], w_empty[8], x_full[MAX_NC], x_empty[MAX_NC], d_full[MAX_NDB], d_empty[MAX_NDB];
-  __shared__ uint64_t pw_full[8], px_full[MAX_NC];  // pairs: the peer's loads, forwarded to the leader
+  // per-chunk X barriers: chunk c of band k+1 is reloaded as soon as both MMA warps' last taps
+  // of band k on chunk c complete, so band transitions overlap the last taps' MMAs
+  __shared__ uint64_t w_full[MAX_STAGES], w_empty[MAX_STAGES], x_full[MAX_NC], x_empty[MAX_NC], d_full[MAX_NDB],
+      d_empty[MAX_NDB];
   __shared__ uint32_t tmem_base_sh;
 
   const int warp = threadIdx.x / 32;
   const int S = p.w_stages;
-  const uint32_t rank = PAIR ? cluster_ctarank() : 0;
   if (threadIdx.x == 0) {
     for (int s = 0; s < S; ++s) {
       mbar_init(&w_full[s], 1);
       mbar_init(&w_empty[s], 1);
-      mbar_init(&pw_full[s], 1);
     }
     for (int i = 0; i < p.NC; ++i) {
       mbar_init(&x_full[i], 1);
-      mbar_init(&x_empty[i], 1);
-      mbar_init(&px_full[i], 1);
+      mbar_init(&x_empty[i], NUM_MMA);  // one commit per MMA warp per band
     }
     for (int i = 0; i < NDB; ++i) {
       mbar_init(&d_full[i], 1);
-      mbar_init(&d_empty[i], PAIR ? 2 * NUM_EPI : NUM_EPI);
+      mbar_init(&d_empty[i], NUM_EPI);
     }
     fence_barrier_init();
   }
-  if (warp == 1) {
-    if constexpr (PAIR)
-      tmem_alloc2<512>(&tmem_base_sh);
-    else
-      tmem_alloc<512>(&tmem_base_sh);
-  }
+  if (warp == 1) tmem_alloc<512>(&tmem_base_sh);
   tc_fence_before();
   __syncthreads();
-  if constexpr (PAIR) cluster_sync_all();  // peer barriers initialised before any remote arrive
   tc_fence_after();
   const uint32_t tmem = tmem_base_sh;
 
@@ -658,114 +504,81 @@ __global__ void __launch_bounds__(THREADS, 1) ri_tc_kernel(const __grid_constant
   const int stage_w = p.spc * parts * WTILE;                      // W bytes of a stage
   const int stage_bytes = stage_w + (p.xstream ? p.spc * parts * XS : 0);
   const int stages_per_tap = p.NC / p.spc;
-  const Work wk = make_work<PAIR>(p);
-  const size_t xoff = PAIR ? rank * XS : 0;  // this CTA's half of every band tile
+  const int S0 = (S + 1) / 2;  // ring 0 (MMA warp 1): slots [0, S0); ring 1 (MMA warp 2): [S0, S)
   if (warp < EPI_WARP0) asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(REGS_PRODUCER));
-  if (warp == 0) {
-    // ------------------------------------------------------------ producer (whole warp
-    // walks the schedule in MMA consumption order; one elected lane issues the copies)
+  if (warp == 0 || warp == 3) {
+    // ------------------------------------------------------------ producers (whole warp
+    // walks the schedule in MMA consumption order; one elected lane issues the copies).
+    // Producer i = warp / 3 fills ring i for the taps of MMA warp i + 1.
+    const uint32_t me = warp == 0 ? 0u : 1u;
+    const int S_me = me == 0 ? S0 : S - S0, base = me == 0 ? 0 : S0;
     Ring wr;
-    uint32_t xc = 0;  // bands loaded so far (phase of the per-chunk X barriers)
-    for (int item = wk.first; item < wk.count; item += wk.stride) {
-      const int n = wk.n(item), ct = wk.ct(item);
-      for (int k = 0; k < p.NBK; ++k)
-        for (int b = 0; b < p.NB; ++b) {
-          const size_t tile = ((size_t)n * p.NBK + k) * p.NC;
-          const uint8_t* wsrc = p.w + (((size_t)b * p.NCT + ct) * 9) * p.NC * parts * WTILE;
-          for (int st = 0; st < 9 * stages_per_tap; ++st) {
-            if (!p.xstream && b == 0 && st < stages_per_tap) {  // new band, tap 0: its X chunks first
-              for (int cl = 0; cl < p.spc; ++cl) {
-                const int c = st * p.spc + cl;
-                if (xc > 0) {
-                  if constexpr (PAIR)
-                    mbar_wait_spin(&x_empty[c], (xc - 1) & 1);
-                  else
-                    mbar_wait(&x_empty[c], (xc - 1) & 1);
-                }
-                if (elect_one()) {
-                  mbar_arrive_expect_tx(&x_full[c], parts * XS);
-                  if (G::CAT && !PAIR && parts == 2) {  // [Xh_c | Xl_c]: one N = 192 B operand
-                    bulk_g2s(xs + 2 * c * XS, p.xh + (tile + c) * XTILE + xoff, XS, &x_full[c]);
-                    bulk_g2s(xs + (2 * c + 1) * XS, p.xl + (tile + c) * XTILE + xoff, XS, &x_full[c]);
-                  } else {
-                    bulk_g2s(xs + c * XS, p.xh + (tile + c) * XTILE + xoff, XS, &x_full[c]);
-                    if (parts == 2) bulk_g2s(xs + (p.NC + c) * XS, p.xl + (tile + c) * XTILE + xoff, XS, &x_full[c]);
-                  }
-                }
-                __syncwarp();
-              }
-            }
-            if (wr.used) {
-              if constexpr (PAIR)
-                mbar_wait_spin(&w_empty[wr.s], wr.ph ^ 1);
-              else
-                mbar_wait(&w_empty[wr.s], wr.ph ^ 1);
-            }
+    uint32_t xc = 0, gd = 0;  // bands loaded so far (phase of the per-chunk X barriers), global tap
+    for (int item = blockIdx.x; item < p.items; item += gridDim.x) {
+      const int n = item / p.NCT, ct = item % p.NCT;
+      for (int k = 0; k < p.NBK; ++k) {
+        const size_t tile = ((size_t)n * p.NBK + k) * p.NC;
+        if (me == 0 && !p.xstream) {  // new band: its X chunks (both MMA warps read them)
+          for (int c = 0; c < p.NC; ++c) {
+            if (xc > 0) mbar_wait(&x_empty[c], (xc - 1) & 1);
             if (elect_one()) {
-              if (p.ablate == 3 || p.ablate == 4 || p.ablate == 6) {
-                mbar_arrive(&w_full[wr.s]);  // profiling: no weight traffic
-              } else {
-                mbar_arrive_expect_tx(&w_full[wr.s], stage_bytes);
-                uint8_t* dst = ws + wr.s * stage_bytes;
-                bulk_g2s(dst, wsrc + (size_t)st * stage_w, stage_w, &w_full[wr.s]);
-                if (p.xstream) {  // the stage's X chunks travel with it (re-read from L2 per tap)
-                  const int c0 = (st % stages_per_tap) * p.spc;
-                  for (int cl = 0; cl < p.spc; ++cl) {
-                    bulk_g2s(dst + stage_w + cl * XS, p.xh + (tile + c0 + cl) * XTILE + xoff, XS, &w_full[wr.s]);
-                    if (parts == 2)
-                      bulk_g2s(dst + stage_w + (p.spc + cl) * XS, p.xl + (tile + c0 + cl) * XTILE + xoff, XS,
-                               &w_full[wr.s]);
-                  }
-                }
-              }
+              mbar_arrive_expect_tx(&x_full[c], parts * XS);
+              bulk_g2s(xs + c * XS, p.xh + (tile + c) * XS, XS, &x_full[c]);
+              if (parts == 2) bulk_g2s(xs + (p.NC + c) * XS, p.xl + (tile + c) * XS, XS, &x_full[c]);
             }
             __syncwarp();
-            wr.adv(S);
           }
-          if (b == p.NB - 1) ++xc;  // the band's X is reloaded only after its last base
         }
-    }
-  } else if (warp == 1 && PAIR && rank != 0) {
-    // ------------------------------------------------------------ pair peer: forward
-    // "this CTA's stage / X chunk landed" to the leader, in the leader's consumption order
-    const uint32_t pw_cl = mapa_shared(pw_full, 0), px_cl = mapa_shared(px_full, 0);
-    Ring wr;
-    uint32_t xc = 0;
-    for (int item = wk.first; item < wk.count; item += wk.stride)
-      for (int k = 0; k < p.NBK; ++k)
         for (int b = 0; b < p.NB; ++b) {
-          for (int t = 0; t < 9; ++t)
+          const uint8_t* wsrc = p.w + (((size_t)b * p.NCT + ct) * 9) * p.NC * parts * WTILE;
+          for (int t = 0; t < 9; ++t, ++gd) {
+            if ((gd & 1u) != me) continue;
             for (int sp = 0; sp < stages_per_tap; ++sp) {
-              if (t == 0 && b == 0 && !p.xstream)
-                for (int cl = 0; cl < p.spc; ++cl) {
-                  const int c = sp * p.spc + cl;
-                  mbar_wait(&x_full[c], xc & 1);
-                  if (elect_one()) mbar_arrive_cluster(px_cl + c * 8);
-                  __syncwarp();
+              const int st = t * stages_per_tap + sp;
+              if (wr.used) mbar_wait(&w_empty[base + wr.s], wr.ph ^ 1);
+              if (elect_one()) {
+                uint64_t* full = &w_full[base + wr.s];
+                mbar_arrive_expect_tx(full, stage_bytes);
+                uint8_t* dst = ws + (base + wr.s) * stage_bytes;
+                bulk_g2s(dst, wsrc + (size_t)st * stage_w, stage_w, full);
+                if (p.xstream) {  // the stage's X chunks travel with it (re-read from L2 per tap)
+                  const int c0 = sp * p.spc;
+                  for (int cl = 0; cl < p.spc; ++cl) {
+                    bulk_g2s(dst + stage_w + cl * XS, p.xh + (tile + c0 + cl) * XS, XS, full);
+                    if (parts == 2) bulk_g2s(dst + stage_w + (p.spc + cl) * XS, p.xl + (tile + c0 + cl) * XS, XS, full);
+                  }
                 }
-              mbar_wait(&w_full[wr.s], wr.ph);
-              if (elect_one()) mbar_arrive_cluster(pw_cl + wr.s * 8);
+              }
               __syncwarp();
-              wr.adv(S);
+              wr.adv(S_me);
             }
-          if (b == p.NB - 1) ++xc;
+          }
         }
-  } else if (warp == 1) {
-    // ------------------------------------------------------------ MMA issuer (whole warp
-    // waits; one elected lane issues tcgen05.mma + commits)
-    const uint32_t idesc = idesc_bf16_f32(PAIR ? 256 : 128, G::MMA_N);
+        ++xc;
+      }
+    }
+  } else if (warp == 1 || warp == 2) {
+    // ------------------------------------------------------------ MMA issuers.  Both warps
+    // walk the whole schedule (ring / buffer / phase state stays in lockstep); warp 1 issues
+    // the even taps of the global tap sequence, warp 2 the odd ones.  Each tap has its own
+    // D buffer and W stages, so the two streams never touch the same accumulator; each warp
+    // commits its own MMAs (tcgen05.commit tracks the issuing thread's operations).
+    const uint32_t me = (uint32_t)(warp - 1);
+    const int S_me = me == 0 ? S0 : S - S0, base = me == 0 ? 0 : S0;
+    const uint32_t idesc = idesc_bf16_f32(128, G::MMA_N);
     const uint32_t xaddr = smem_u32(xs);
+    const int taps_per_band = p.NB * 9;
     Ring wr;
-    uint32_t xc = 0, gd = 0, areg = 0;
+    uint32_t xc = 0, gd = 0;  // gd: global tap index
     int db = 0;
     uint32_t dph = 0;
-    for (int item = wk.first; item < wk.count; item += wk.stride) {
+    for (int item = blockIdx.x; item < p.items; item += gridDim.x) {
       for (int k = 0; k < p.NBK; ++k) {
         // full-row bands at the image top / bottom: the halo rows outside the image are zero
         // padding, so the MMA skips them (N shrinks by RS per row; the epilogue never reads
         // them, see band_rows)
         uint32_t idesc_k = idesc, xoff_k = 0, doff_k = 0;
-        if (TRIM && p.trim) {
+        if constexpr (G::TRIM) {
           const int2 v = band_rows<TW>(k, p.H);
           idesc_k = idesc_bf16_f32(128, (uint32_t)((v.y - v.x) * G::RS));
           xoff_k = (uint32_t)(v.x * G::RS * 128);
@@ -773,110 +586,49 @@ __global__ void __launch_bounds__(THREADS, 1) ri_tc_kernel(const __grid_constant
         }
         for (int b = 0; b < p.NB; ++b) {
           for (int t = 0; t < 9; ++t) {
-            if (gd >= NDB) {
-              if constexpr (PAIR)
-                mbar_wait_spin(&d_empty[db], dph ^ 1);  // completed by the peer's epilogue too
-              else
-                mbar_wait(&d_empty[db], dph ^ 1);
-            }
-            tc_fence_after();
-            const uint32_t d = tmem + G::D0 + db * G::DCOLS + doff_k;
-            for (int sp = 0; sp < stages_per_tap; ++sp) {
-              if (t == 0 && b == 0 && !p.xstream)
-                for (int cl = 0; cl < p.spc; ++cl) {
-                  mbar_wait(&x_full[sp * p.spc + cl], xc & 1);
-                  if constexpr (PAIR) mbar_wait_spin(&px_full[sp * p.spc + cl], xc & 1);
-                }
-              mbar_wait(&w_full[wr.s], wr.ph);
-              if constexpr (PAIR) mbar_wait_spin(&pw_full[wr.s], wr.ph);
+            const int tb = b * 9 + t;                       // tap index within the band
+            const bool mine = (gd & 1u) == me;
+            const bool first_mine = tb < 2;                 // this warp's first tap of the band
+            const bool last_mine = tb + 2 >= taps_per_band;  // ... and its last one
+            if (mine) {
+              if (gd >= (uint32_t)NDB) mbar_wait(&d_empty[db], dph ^ 1);
               tc_fence_after();
-              if (elect_one()) {
-                const uint32_t wbase = smem_u32(ws + wr.s * stage_bytes);
-                // descriptors are linear in the smem address (14-bit field, smem < 256 KB): one
-                // base per stage, constant strides per chunk (with the 64-register MMA warp this
-                // denser issue is 1% faster; at 32 registers it was 8-12% slower)
-                const bool cat = G::CAT && !PAIR && parts == 2 && !p.xstream;
-                const uint32_t xstride = cat ? 2 * XS : XS;  // X chunk c: resident band tile or the stage's copy
-                const uint32_t xbase = p.xstream ? wbase + stage_w : xaddr + sp * p.spc * xstride;
-                const uint32_t lo_off = cat ? XS : (p.xstream ? p.spc * XS : p.NC * XS);
-                const uint64_t b0 = desc_k_sw128(xbase + xoff_k), a0 = desc_k_sw128(wbase);
-                for (int cl = 0; cl < ((p.ablate == 2 || p.ablate == 3) ? 0 : p.spc); ++cl) {
-                  const int c = sp * p.spc + cl;
-                  const uint32_t xh_a = xbase + cl * xstride, xl_a = xh_a + lo_off;
-                  const uint64_t bh = b0 + (uint32_t)((cl * xstride) >> 4);
-                  const uint64_t ah = a0 + (uint32_t)((cl * parts * WTILE) >> 4);
-                  if (G::CAT && !PAIR && cat) {
-                    const uint32_t idesc2 = idesc_bf16_f32(128, 2 * G::MMA_N);
-                    const uint64_t al = desc_k_sw128(wbase + (cl * parts + 1) * WTILE);
+              const uint32_t d = tmem + G::D0 + db * G::DCOLS + doff_k;
+              for (int sp = 0; sp < stages_per_tap; ++sp) {
+                if (first_mine && !p.xstream)
+                  for (int cl = 0; cl < p.spc; ++cl) mbar_wait(&x_full[sp * p.spc + cl], xc & 1);
+                mbar_wait(&w_full[base + wr.s], wr.ph);
+                tc_fence_after();
+                if (elect_one()) {
+                  const uint32_t wbase = smem_u32(ws + (base + wr.s) * stage_bytes);
+                  // descriptors are linear in the smem address (14-bit field, smem < 256 KB): one
+                  // base per stage, constant strides per chunk
+                  const uint32_t xbase = p.xstream ? wbase + stage_w : xaddr + sp * p.spc * XS;
+                  const uint32_t lo_off = p.xstream ? p.spc * XS : p.NC * XS;
+                  const uint64_t b0 = desc_k_sw128(xbase + xoff_k), a0 = desc_k_sw128(wbase);
+                  for (int cl = 0; cl < p.spc; ++cl) {
+                    const int c = sp * p.spc + cl;
+                    const uint32_t xh_a = xbase + cl * XS, xl_a = xh_a + lo_off;
+                    const uint64_t bh = b0 + (uint32_t)((cl * XS) >> 4);
+                    const uint64_t ah = a0 + (uint32_t)((cl * parts * WTILE) >> 4);
 #pragma unroll
-                    for (int kk = 0; kk < 4; ++kk) mma_bf16_ss(d, ah + 2 * kk, bh + 2 * kk, idesc2, (c | kk) != 0);
+                    for (int kk = 0; kk < 4; ++kk) mma_bf16_ss(d, ah + 2 * kk, bh + 2 * kk, idesc_k, (c | kk) != 0);
+                    if (parts == 2) {
+                      const uint64_t bl = desc_k_sw128(xl_a + xoff_k);
+                      const uint64_t al = desc_k_sw128(wbase + (cl * parts + 1) * WTILE);
 #pragma unroll
-                    for (int kk = 0; kk < 4; ++kk) mma_bf16_ss(d, al + 2 * kk, bh + 2 * kk, idesc_k, 1);
-                  } else if (kTsa && !PAIR && parts == 2) {
-                    const uint32_t atm = tmem + A_COL0 + (areg++ & 1) * 32;
+                      for (int kk = 0; kk < 4; ++kk) mma_bf16_ss(d, ah + 2 * kk, bl + 2 * kk, idesc_k, 1);
 #pragma unroll
-                    for (int kk = 0; kk < 4; ++kk) tmem_cp_128x256b(atm + 8 * kk, ah + 2 * kk);
-#pragma unroll
-                    for (int kk = 0; kk < 4; ++kk) mma_bf16_ts(d, atm + 8 * kk, bh + 2 * kk, idesc_k, (c | kk) != 0);
-                    const uint64_t bl = desc_k_sw128(xl_a + xoff_k);
-                    const uint64_t al = desc_k_sw128(wbase + (cl * parts + 1) * WTILE);
-#pragma unroll
-                    for (int kk = 0; kk < 4; ++kk) mma_bf16_ts(d, atm + 8 * kk, bl + 2 * kk, idesc_k, 1);
-#pragma unroll
-                    for (int kk = 0; kk < 4; ++kk) mma_bf16_ss(d, al + 2 * kk, bh + 2 * kk, idesc_k, 1);
-                  } else {
-#pragma unroll
-                  for (int kk = 0; kk < 4; ++kk) {
-                    if constexpr (PAIR)
-                      mma_bf16_ss_pair(d, ah + 2 * kk, bh + 2 * kk, idesc, (c | kk) != 0);
-                    else
-                      mma_bf16_ss(d, ah + 2 * kk, bh + 2 * kk, idesc_k, (c | kk) != 0);
-                  }
-                  if (parts == 2) {
-                    const uint64_t bl = desc_k_sw128(xl_a + xoff_k);
-                    const uint64_t al = desc_k_sw128(wbase + (cl * parts + 1) * WTILE);
-#pragma unroll
-                    for (int kk = 0; kk < 4; ++kk) {
-                      if constexpr (PAIR)
-                        mma_bf16_ss_pair(d, ah + 2 * kk, bl + 2 * kk, idesc, 1);
-                      else
-                        mma_bf16_ss(d, ah + 2 * kk, bl + 2 * kk, idesc_k, 1);
+                      for (int kk = 0; kk < 4; ++kk) mma_bf16_ss(d, al + 2 * kk, bh + 2 * kk, idesc_k, 1);
                     }
-#pragma unroll
-                    for (int kk = 0; kk < 4; ++kk) {
-                      if constexpr (PAIR)
-                        mma_bf16_ss_pair(d, al + 2 * kk, bh + 2 * kk, idesc, 1);
-                      else
-                        mma_bf16_ss(d, al + 2 * kk, bh + 2 * kk, idesc_k, 1);
-                    }
+                    if (last_mine && !p.xstream) mma_commit(&x_empty[c]);  // chunk c done by this warp
                   }
-                  }
-                  if (t == 8 && b == p.NB - 1 && !p.xstream) {  // chunk c of this band fully consumed
-                    if constexpr (PAIR)
-                      mma_commit_pair(&x_empty[c], 0x3);
-                    else
-                      mma_commit(&x_empty[c]);
-                  }
-                }
-                if ((p.ablate == 2 || p.ablate == 3) && !p.xstream) {
-                  if (t == 8 && b == p.NB - 1)
-                    for (int cl = 0; cl < p.spc; ++cl) {
-                      if constexpr (PAIR)
-                        mma_commit_pair(&x_empty[sp * p.spc + cl], 0x3);
-                      else
-                        mma_commit(&x_empty[sp * p.spc + cl]);
-                    }
-                }
-                if constexpr (PAIR) {
-                  mma_commit_pair(&w_empty[wr.s], 0x3);
-                  if (sp == stages_per_tap - 1) mma_commit_pair(&d_full[db], 0x3);
-                } else {
-                  mma_commit(&w_empty[wr.s]);
+                  mma_commit(&w_empty[base + wr.s]);
                   if (sp == stages_per_tap - 1) mma_commit(&d_full[db]);
                 }
+                __syncwarp();
+                wr.adv(S_me);
               }
-              __syncwarp();
-              wr.adv(S);
             }
             ++gd;
             if (++db == NDB) {
@@ -891,17 +643,13 @@ __global__ void __launch_bounds__(THREADS, 1) ri_tc_kernel(const __grid_constant
   } else if (warp >= EPI_WARP0) {
     // ------------------------------------------------------------ epilogue
     asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(REGS_EPILOGUE));
-    epilogue<TW, RPB, CONV, PAIR>(p, tmem, d_full, d_empty);
+    epilogue<TW, RPB, CONV>(p, tmem, d_full, d_empty);
   }
   tc_fence_before();
   __syncthreads();
-  if constexpr (PAIR) {
-    cluster_sync_all();  // no remote arrive / pair MMA may target a CTA that has left
-    if (warp == 1) tmem_dealloc2<512>(tmem);
-  } else {
-    if (warp == 1) tmem_dealloc<512>(tmem);
-  }
+  if (warp == 1) tmem_dealloc<512>(tmem);
 }
+
 
 // ---- packing kernels ------------------------------------------------------------------
 __device__ __forceinline__ void split_bf16(float v, __nv_bfloat16& hi, __nv_bfloat16& lo) {
@@ -983,23 +731,18 @@ __global__ void w_pack_kernel(const float* __restrict__ bases, uint8_t* __restri
 }
 
 struct TcGeom {
-  int gi;       // geometry: 0 = TW 16, 1 = TW 32, 2 = strips, 3 = 8x8 images, 4 = 4x4 images
+  int gi;       // geometry: 0 = TW 16, 2 = strips, 3 = 8x8 images, 4 = 4x4 images
   int units;    // band owners: images, or bands of IMGS small images
   int NBK, NC, NCT, xtile;
   size_t x_plane, w_plane;
 };
 TcGeom geom(const rc_desc& d) {
   TcGeom g;
-  g.gi = d.w == 16 ? 0 : d.w == 32 ? 1 : (d.w == 8 && d.h == 8) ? 3 : (d.w == 4 && d.h == 4) ? 4 : 2;
-  if (g.gi == 1) {
-    // W = 32 runs as two 4x16 strips per 4 rows (N = 112, 1.69 input px per output px)
-    // rather than 2-row bands (N = 128, 2.0): 5-8% faster on C4 (profiles/r01/strip32.txt).
-    // RC_TC_ROWS32=1 selects the 2-row bands (A/B testing).
-    const char* e = getenv("RC_TC_ROWS32");
-    if (!(e && e[0] == '1')) g.gi = 2;
-  }
-  static const int out_rows_of[5] = {Geo<16>::OUT_ROWS, Geo<32>::OUT_ROWS, Geo<0>::OUT_ROWS, 8, 4};
-  static const int xtile_of[5] = {Geo<16>::XTILE, Geo<32>::XTILE, Geo<0>::XTILE, Geo<8>::XTILE, Geo<4>::XTILE};
+  // W = 32 runs as two 4x16 strips per 4 rows (N = 112, 1.69 input px per output px); 2-row
+  // bands (N = 128, 2.0) were 5-8% slower on C4 (profiles/r01/strip32.txt)
+  g.gi = d.w == 16 ? 0 : (d.w == 8 && d.h == 8) ? 3 : (d.w == 4 && d.h == 4) ? 4 : 2;
+  static const int out_rows_of[5] = {Geo<16>::OUT_ROWS, 0, Geo<0>::OUT_ROWS, 8, 4};
+  static const int xtile_of[5] = {Geo<16>::XTILE, 0, Geo<0>::XTILE, Geo<8>::XTILE, Geo<4>::XTILE};
   g.xtile = xtile_of[g.gi];
   g.units = g.gi == 3 ? d.n : (g.gi == 4 ? (d.n + 3) / 4 : d.n);
   g.NBK = g.gi >= 3 ? 1 : (d.h + out_rows_of[g.gi] - 1) / out_rows_of[g.gi] * (g.gi == 2 ? d.w / 16 : 1);
@@ -1014,40 +757,42 @@ struct SmemPlan {
   int spc, stages, xstream;
   size_t bytes;
 };
-// Preferred: one resident X band (per-chunk barriers overlap its reload with the last tap)
-// plus the largest W stage (chunks per stage dividing NC) that leaves >= 2 stages.  When the
-// band does not fit (large Cin), X chunks are streamed with the W stages instead (X re-read
-// from L2 once per tap).
-SmemPlan smem_plan(const TcGeom& g, int parts, bool pair = false) {
+// Preferred: one resident X band (per-chunk barriers overlap its reload with the last taps)
+// plus a W ring of single-chunk stages (one chunk = one tap's 64 input channels, hi + lo)
+// as deep as shared memory allows: with two MMA warps working on consecutive taps, small
+// stages let the next tap's chunks land as the current tap frees its slots.  When the band
+// does not fit (large Cin), X chunks are streamed with the W stages instead (X re-read from
+// L2 once per tap).
+SmemPlan smem_plan(const TcGeom& g, int parts) {
   SmemPlan sp{0, 0, 0, 0};
   const size_t cap = 232448 - 1024 - 1024;  // dynamic smem minus alignment slack / statics
-  const size_t xt = pair ? g.xtile / 2 : g.xtile;  // a CTA of a pair holds half of every band tile
+  const size_t xt = g.xtile;
   const size_t xbuf = (size_t)parts * g.NC * xt;
   const size_t chunk = (size_t)parts * WTILE;
-  // fewest stages wanted in the W ring: a pair's leader waits on the peer's forwarded
-  // "stage landed" event too, so it needs a deeper prefetch
-  const char* ms = getenv("RC_TC_MIN_STAGES");
-  const size_t min_stages = ms ? (size_t)atoi(ms) : 2;
   if (g.NC <= MAX_NC && xbuf < cap) {
     const size_t budget = cap - xbuf;
+    // the two MMA warps each own a ring of >= 2 stages: the largest stage (the TMA engine's
+    // per-copy cost favours big copies, profiles/r01/wstage_ab.txt) for which 4 stages fit,
+    // then as many stages as fit; single-chunk stages, >= 1 per ring, at the least
     for (int c = g.NC; c >= 1; --c) {
       if (g.NC % c) continue;
       const size_t sb = c * chunk;
-      if (min_stages * sb <= budget || (c == 1 && 2 * sb <= budget)) {
+      const size_t n = budget / sb;
+      if (n >= 4 || (c == 1 && n >= 2)) {
         sp.spc = c;
-        sp.stages = (int)(budget / sb) > 8 ? 8 : (int)(budget / sb);
+        sp.stages = n > MAX_STAGES ? MAX_STAGES : (int)n;
         sp.bytes = xbuf + sp.stages * sb + 1024;
         return sp;
       }
     }
   }
   const size_t schunk = (size_t)parts * (WTILE + xt);
-  for (int c = g.NC; c >= 1; --c) {
+  for (int c = 1; c <= g.NC; ++c) {
     if (g.NC % c) continue;
     const size_t sb = c * schunk;
-    if (3 * sb <= cap || (c == 1 && 2 * sb <= cap)) {
+    if (4 * sb <= cap || (c == 1 && 2 * sb <= cap)) {
       sp.spc = c;
-      sp.stages = (int)(cap / sb) > 8 ? 8 : (int)(cap / sb);
+      sp.stages = (int)(cap / sb) > MAX_STAGES ? MAX_STAGES : (int)(cap / sb);
       sp.xstream = 1;
       sp.bytes = sp.stages * sb + 1024;
       return sp;
@@ -1110,7 +855,7 @@ int launch_tc(const rc_desc& d, const float* x, const void* bank, const float* b
   if (!band_supported(d)) return RC_ERR_UNSUPPORTED;
   if (name) {
     static const char* names[5][2] = {{"tc_k3w16_bf16x3", "tc_k3w16_bf16"},
-                                      {"tc_k3w32_bf16x3", "tc_k3w32_bf16"},
+                                      {"", ""},
                                       {"tc_k3strip_bf16x3", "tc_k3strip_bf16"},
                                       {"tc_k3img8_bf16x3", "tc_k3img8_bf16"},
                                       {"tc_k3img4_bf16x3", "tc_k3img4_bf16"}};
@@ -1128,7 +873,6 @@ int launch_tc(const rc_desc& d, const float* x, const void* bank, const float* b
   const dim3 pgrid(g.NC, g.NBK, g.units);
   switch (gi) {
     case 0: x_pack_kernel<16><<<pgrid, 256, 0, s>>>(x, xh, xl, d.c_in, d.h, d.w, g.NBK, g.NC, d.n); break;
-    case 1: x_pack_kernel<32><<<pgrid, 256, 0, s>>>(x, xh, xl, d.c_in, d.h, d.w, g.NBK, g.NC, d.n); break;
     case 2: x_pack_kernel<0><<<pgrid, 256, 0, s>>>(x, xh, xl, d.c_in, d.h, d.w, g.NBK, g.NC, d.n); break;
     case 3: x_pack_kernel<8><<<pgrid, 256, 0, s>>>(x, xh, xl, d.c_in, d.h, d.w, g.NBK, g.NC, d.n); break;
     default: x_pack_kernel<4><<<pgrid, 256, 0, s>>>(x, xh, xl, d.c_in, d.h, d.w, g.NBK, g.NC, d.n); break;
@@ -1136,13 +880,7 @@ int launch_tc(const rc_desc& d, const float* x, const void* bank, const float* b
   RC_CUDA(cudaGetLastError());
   const BankLayout L = bank_layout(d);
   const uint8_t* tcb = static_cast<const uint8_t*>(bank) + L.tc_off;
-  // CTA pairs (cta_group::2) for the N = 96 band of 16-wide images: bit-exact, but measured
-  // SLOWER than single CTAs on C3 (2.75 vs 2.28 ms bf16x3, profiles/r01/pair_ablation.txt):
-  // the pair's load/forward/release chain costs more than the halved B-operand traffic
-  // saves.  Kept behind RC_TC_PAIR=1 for experiments; off by default.
-  const char* pe = getenv("RC_TC_PAIR");
-  const bool pair = d.w == 16 && g.NCT % 2 == 0 && pe && pe[0] == '1';
-  const SmemPlan plan = smem_plan(g, parts, pair);
+  const SmemPlan plan = smem_plan(g, parts);
   TcParams p;
   p.xh = xh;
   p.xl = xl;
@@ -1168,54 +906,19 @@ int launch_tc(const rc_desc& d, const float* x, const void* bank, const float* b
   p.spc = plan.spc;
   p.xstream = plan.xstream;
   p.items = g.NCT * g.units;
-  {
-    const char* ab = getenv("RC_TC_ABLATE");  // profiling switch, see TcParams::ablate
-    p.ablate = ab ? atoi(ab) : 0;
-    const char* tr = getenv("RC_TC_TRIM");
-    p.trim = tr ? atoi(tr) : 1;
-  }
   int dev, sms;
   RC_CUDA(cudaGetDevice(&dev));
   RC_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
   // [geometry][single][convention]
   static void (*const kernels[5][2][2])(TcParams) = {
-      {{ri_tc_kernel<16, 4, 0, false>, ri_tc_kernel<16, 4, 1, false>},
-       {ri_tc_kernel<16, 1, 0, false>, ri_tc_kernel<16, 1, 1, false>}},
-      {{ri_tc_kernel<32, 4, 0, false>, ri_tc_kernel<32, 4, 1, false>},
-       {ri_tc_kernel<32, 1, 0, false>, ri_tc_kernel<32, 1, 1, false>}},
-      {{ri_tc_kernel<0, 4, 0, false>, ri_tc_kernel<0, 4, 1, false>},
-       {ri_tc_kernel<0, 1, 0, false>, ri_tc_kernel<0, 1, 1, false>}},
-      {{ri_tc_kernel<8, 4, 0, false>, ri_tc_kernel<8, 4, 1, false>},
-       {ri_tc_kernel<8, 1, 0, false>, ri_tc_kernel<8, 1, 1, false>}},
-      {{ri_tc_kernel<4, 4, 0, false>, ri_tc_kernel<4, 4, 1, false>},
-       {ri_tc_kernel<4, 1, 0, false>, ri_tc_kernel<4, 1, 1, false>}}};
-  static void (*const pair_kernels[2][2])(TcParams) = {
-      {ri_tc_kernel<16, 4, 0, true>, ri_tc_kernel<16, 4, 1, true>},
-      {ri_tc_kernel<16, 1, 0, true>, ri_tc_kernel<16, 1, 1, true>}};
+      {{ri_tc_kernel<16, 4, 0>, ri_tc_kernel<16, 4, 1>}, {ri_tc_kernel<16, 1, 0>, ri_tc_kernel<16, 1, 1>}},
+      {{nullptr, nullptr}, {nullptr, nullptr}},
+      {{ri_tc_kernel<0, 4, 0>, ri_tc_kernel<0, 4, 1>}, {ri_tc_kernel<0, 1, 0>, ri_tc_kernel<0, 1, 1>}},
+      {{ri_tc_kernel<8, 4, 0>, ri_tc_kernel<8, 4, 1>}, {ri_tc_kernel<8, 1, 0>, ri_tc_kernel<8, 1, 1>}},
+      {{ri_tc_kernel<4, 4, 0>, ri_tc_kernel<4, 4, 1>}, {ri_tc_kernel<4, 1, 0>, ri_tc_kernel<4, 1, 1>}}};
   const int single = d.group == RC_GROUP_SINGLE, raw = d.convention == RC_CONV_RAW;
-  void (*fn)(TcParams) = pair ? pair_kernels[single][raw] : kernels[gi][single][raw];
+  void (*fn)(TcParams) = kernels[gi][single][raw];
   RC_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)plan.bytes));
-  if (pair) {
-    const int pairs = p.items / 2;  // pair items = N * NCT / 2
-    const int clusters = pairs < sms / 2 ? pairs : sms / 2;
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(2 * clusters);
-    cfg.blockDim = dim3(THREADS);
-    cfg.dynamicSmemBytes = plan.bytes;
-    cfg.stream = s;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = 2;
-    attr[0].val.clusterDim.y = 1;
-    attr[0].val.clusterDim.z = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    prof_begin(s);
-    RC_CUDA(cudaLaunchKernelEx(&cfg, fn, p));
-    prof_end(s);
-    RC_CUDA(cudaGetLastError());
-    return RC_OK;
-  }
   const int grid = p.items < sms ? p.items : sms;
   prof_begin(s);
   fn<<<grid, THREADS, plan.bytes, s>>>(p);

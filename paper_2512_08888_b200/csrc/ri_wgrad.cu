@@ -274,8 +274,7 @@ WgGeom wg_geom(const rc_desc& d) {
   g.MT = (g.M + 127) / 128;
   // 128-ci tiles (N = 128: math-bound MMAs, 3 taps x 128 TMEM columns) when the planes pair
   // up, else 64-ci tiles (N = 64: shared-memory bound, 5 + 4 taps); RC_WGRAD_N=64 forces 64
-  const char* en = getenv("RC_WGRAD_N");
-  g.nci = (pg.NC % 2 == 0 && !(en && atoi(en) == 64)) ? 2 : 1;
+  g.nci = pg.NC % 2 == 0 ? 2 : 1;  // 128-ci tiles where Cin allows (profiles/r01/bwd_wgrad_ab.txt)
   g.parts = d.precision == RC_PREC_BF16 ? 1 : 2;
   g.xr = (KQ + 2 * (pg.Wp + 1) + 7 + 7) / 8 * 8;
   const size_t cap0 = 232448 - 1024 - 512;
@@ -308,8 +307,6 @@ size_t al256(size_t v) { return (v + 255) & ~size_t(255); }
 }  // namespace
 
 bool wgrad_supported(const rc_desc& d) {
-  const char* e = getenv("RC_BWD_TC");  // A/B switch (default on)
-  if (e && e[0] == '0') return false;
   if (d.k != 3 || d.precision == RC_PREC_FP32) return false;
   return wg_geom(d).stages >= 2;
 }
