@@ -160,62 +160,92 @@ class ClockSampler:
                 "source": "nvml" if self.nvml is not None else "nvidia-smi"}
 
 
-def cpu_reference(wl, threads: int, target_s: float = 12.0):
-    """The CPU path on a bounded image sample (oracle port of the reuse algorithm; for R=1
-    the unmodified reference tiled_scatter_conv).  Returns (eff TFLOP/s, dict)."""
+def cpu_reference(wl, threads: int, target_s: float = 12.0, kind: str = "reference", m0: int | None = None):
+    """The CPU path on a bounded image sample, timed on this host with every core.
+
+    kind "reference": the reference's own code -- the unmodified tiled_scatter_conv
+    (scatter_conv.hpp:330-368, compiled from /root/reference by oracle/Makefile into
+    oracle/_ref) once per orientation slice (R x tiled_scatter_conv: the reference has no
+    reuse path), plus the SPEC pooling and bias (oracle/ref_shim.cpp ref_ri_batch_f).
+    kind "port": the oracle's C restatement of the paper's reuse loop (one dot per tap,
+    scattered to the 4 rotations; bit-identical to the reference slices,
+    tests/test_oracle_ref.py).  The sample starts at m0 (default: one image per thread) and
+    doubles until it takes >= target_s / 4.  Returns (eff TFLOP/s, dict)."""
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
     import oracle as O
     n, cin, h, w, cout, k, g, R, pool, pg, _ = wl
     rng = np.random.default_rng(0)
     s = 1 / np.sqrt(cin * k * k)
-    kind = "reference" if (g == "single" and O.ref_available()) else "port"
+    if kind == "reference" and not O.ref_available():
+        kind = "port"
+    fx = rng.uniform(-s, s, (cout, cin, k, k)).astype(np.float32)
+    fy = rng.uniform(-s, s, (cout, cin, k, k)).astype(np.float32)
+    bias = rng.uniform(-0.1, 0.1, cout).astype(np.float32)
 
     def run(m):
         x = rng.uniform(-1, 1, (m, cin, h, w)).astype(np.float32)
-        fx = rng.uniform(-s, s, (cout, cin, k, k)).astype(np.float32)
-        fy = rng.uniform(-s, s, (cout, cin, k, k)).astype(np.float32)
+        d = O.Desc(m, cin, h, w, cout, k, g, R, pool, pg)
         t0 = time.perf_counter()
         if kind == "reference":
-            O.ref_tiled_batch(x, fx, threads, (0, m))
+            O.ref_ri_batch(d, x, fx, fy, bias, nthreads=threads)
         else:
-            O.ri_forward(O.Desc(m, cin, h, w, cout, k, g, R, pool, pg), x, fx, fy, nthreads=threads)
+            O.ri_forward(d, x, fx, fy, bias, nthreads=threads)
         return time.perf_counter() - t0
 
-    m = threads
-    dt = run(m)  # one image per thread
+    m = m0 or threads
+    dt = run(m)
     while dt < target_s / 4 and m < n:
         m = min(n, m * 2)
         dt = run(m)
     eff = 2.0 * m * h * w * k * k * cin * cout * R
-    return eff / dt / 1e12, {"cores": threads, "kind": kind,
-                             "sample": f"{m} of {n} images x all {cout} output channels "
-                                       f"({dt:.2f} s), linear in images",
+    what = ("R x unmodified tiled_scatter_conv per image + SPEC pooling/bias (oracle/_ref)" if kind == "reference"
+            else "oracle C port of the reuse loop (oracle/librc_oracle.so)")
+    return eff / dt / 1e12, {"cores": threads, "kind": kind, "images": m, "sample_s": dt,
+                             "sample": f"{m} of {n} images x all {cout} output channels in {dt:.2f} s on "
+                                       f"{threads} threads: {what}",
                              "ms_full_layer_extrapolated": dt * n / m * 1e3}
 
 
+def workload_config(args, wl, world: int) -> dict:
+    """The workload a line is quoted on -- identical in both arms (ours and --impl reference)."""
+    n, cin, h, w, cout, k, g, R, pool, pg, label = wl
+    strong = args.workload in STRONG
+    return {"workload": label, "global_batch": n if strong else n * world,
+            "n_per_gpu": -(-n // world) if strong else n, "c_in": cin, "h": h, "w": w, "c_out": cout, "k": k,
+            "group": g, "orientations": R, "pool": pool, "pool_group": pg,
+            "parallelism": f"batch-sharded dp{world}"}
+
+
 def run_reference(args, wl):
+    """--impl reference: the reference's own CPU implementation of the path on this host's
+    cores (rank 0 only), every step a bounded sample of the workload (one image per host
+    thread, R x tiled_scatter_conv each), same metric / unit / config as our arm."""
     rank = int(os.environ.get("RANK", 0))
     if rank != 0:
         return
+    world = int(os.environ.get("WORLD_SIZE", args.gpus))
     threads = os.cpu_count() or 1
-    vals = []
-    info = None
+    vals, secs, info = [], [], None
     for i in range(args.warmup + args.steps):
-        v, info = cpu_reference(wl, threads, target_s=4.0)
+        v, info = cpu_reference(wl, threads, target_s=0.0, kind="reference")
         if i >= args.warmup:
             vals.append(v)
+            secs.append(info["sample_s"])
     v = statistics.median(vals)
-    n, cin, h, w, cout, k, g, R, pool, pg, label = wl
+    ms = statistics.median(secs) * 1e3
     out = {"impl": "reference", "metric": "RI-conv layer effective TFLOP/s", "value": v,
            "unit": "TFLOP/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-           "ms_per_step": info["ms_full_layer_extrapolated"], "higher_is_better": True,
+           "ms_per_step": ms, "ms_per_step_is": f"measured wall time of one step = a {info['images']}-image sample",
+           "ms_full_layer_extrapolated": info["ms_full_layer_extrapolated"] * (world if args.workload not in STRONG else 1),
+           "higher_is_better": True,
            "scaling": "strong" if args.workload in STRONG else "weak", "vs_baseline": None,
-           "dtype": "f32", "data": "synthetic",
-           "config": {"workload": label, "n": n, "orientations": R, "host_threads": threads,
-                      "note": "one host runs the whole workload (the reference has no GPUs)"},
+           "dtype": "f32", "data": "synthetic (uniform[-1,1) inputs, uniform/sqrt(Cin*K^2) weights, random init)",
+           "config": workload_config(args, wl, world),
            "cpu_baseline": {"value": v, "unit": "TFLOP/s", "cores": threads, "kind": info["kind"],
                             "sample": info["sample"]},
-           "e2e": {"value": v, "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+           "e2e": {"value": v, "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+           "note": "the reference has no GPU path: one host runs it; value = effective FLOPs of the sample / its "
+                   "wall time (rate is linear in images)"}
     print(json.dumps(out), flush=True)
 
 
@@ -329,6 +359,13 @@ def _stack_cpu_sample(threads, n_img=2):
     return stack, dt, n_img
 
 
+def stack_config(args, wl, world: int) -> dict:
+    """C5 workload config -- identical in both arms."""
+    return {"workload": wl[-1], "global_batch": wl[0], "batch_per_gpu": -(-wl[0] // world),
+            "image": "3x64x64", "widths": [64, 128, 256], "orientations": 8, "pool": "subgroup", "pool_group": 4,
+            "parallelism": f"batch-sharded dp{world}"}
+
+
 def run_stack_reference(args, wl):
     rank = int(os.environ.get("RANK", 0))
     if rank != 0:
@@ -345,7 +382,7 @@ def run_stack_reference(args, wl):
            "unit": "TFLOP/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
            "ms_per_step": stack.eff_flops(n) / (v * 1e12) * 1e3, "higher_is_better": True,
            "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-           "config": {"workload": wl[-1], "global_batch": n, "host_threads": threads},
+           "config": stack_config(args, wl, int(os.environ.get("WORLD_SIZE", args.gpus))),
            "cpu_baseline": {"value": v, "unit": "TFLOP/s", "cores": threads, "kind": "port",
                             "sample": "2 images through the whole stack, linear in images"},
            "e2e": {"value": v, "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
@@ -447,10 +484,9 @@ def run_stack(args, wl):
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
             "dtype": "mixed: " + ", ".join(sorted({arith_dtype(k) for k in stack.kernels(n)})),
             "data": "synthetic (uniform[-1,1) images, random-init weights)",
-            "config": {"workload": wl[-1], "global_batch": n_total, "batch_per_gpu": n,
-                       "precision": args.precision, "kernels": stack.kernels(n),
-                       "l2": "flushed between timed iterations (512 MB write)",
-                       "parallelism": f"batch-sharded dp{world}", "cuda_graph": True},
+            "config": stack_config(args, wl, world),
+            "precision": args.precision, "kernels": stack.kernels(n), "cuda_graph": True,
+            "l2": "flushed between timed iterations (512 MB write)",
             "alg_tflops": stack.alg_flops(n_total) / (ms * 1e-3) / 1e12,
             "layer_ms": [round(t, 4) for t, _ in layer_ms],
             "roofline": {"bound": "tensor" if top.kernel_name().startswith("tc_") else "fp32-simt",
@@ -605,9 +641,15 @@ def main():
         bwd = backward_context(P, desc, x, bank, y, am)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        v, info = cpu_reference(wl, os.cpu_count() or 1)
+        threads = os.cpu_count() or 1
+        v, info = cpu_reference(wl, threads, target_s=8.0, kind="reference")
         cpu = {"value": v, "unit": "TFLOP/s", "cores": info["cores"], "kind": info["kind"],
                "sample": info["sample"], "ms_full_layer_extrapolated": info["ms_full_layer_extrapolated"]}
+        if R > 1:  # second row: the paper's reuse algorithm on the CPU (same sample size)
+            vp, ip = cpu_reference(wl, threads, target_s=0.0, kind="port", m0=info["images"])
+            cpu["port_reuse"] = {"value": vp, "unit": "TFLOP/s", "cores": ip["cores"], "kind": ip["kind"],
+                                 "sample": ip["sample"],
+                                 "ms_full_layer_extrapolated": ip["ms_full_layer_extrapolated"]}
     if rank == 0:
         out = {
             "metric": "RI-conv layer effective TFLOP/s", "value": value, "unit": "TFLOP/s",
@@ -615,11 +657,9 @@ def main():
             "higher_is_better": True, "scaling": "strong" if strong else "weak", "vs_baseline": None,
             "dtype": arith_dtype(desc.kernel_name()),
             "data": "synthetic (uniform[-1,1) inputs, uniform/sqrt(Cin*K^2) weights, random init)",
-            "config": {"workload": label, "n_per_gpu": n, "global_batch": n_global, "c_in": cin, "h": h, "w": w,
-                       "c_out": cout, "k": k, "group": g, "orientations": R, "pool": pool,
-                       "pool_group": pg, "precision": args.precision, "kernel": desc.kernel_name(),
-                       "l2": "flushed between timed iterations (512 MB write)",
-                       "parallelism": f"batch-sharded dp{world}"},
+            "config": workload_config(args, wl, world),
+            "precision": args.precision, "kernel": desc.kernel_name(),
+            "l2": "flushed between timed iterations (512 MB write)",
             "alg_tflops": achieved * 1.0, "eff_tflops_per_gpu": value / world,
             "roofline": {"bound": "tensor" if tc else "fp32-simt", "kernel": desc.kernel_name(),
                          "achieved": achieved, "peak": tpeak if tc else 74.4, "unit": "TFLOP/s",

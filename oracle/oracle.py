@@ -321,6 +321,29 @@ def ref_ri_slices(d: Desc, x: np.ndarray, w0: np.ndarray, bases: np.ndarray | No
     return f
 
 
+def ref_ri_batch(d: Desc, x: np.ndarray, w0: np.ndarray, w1: np.ndarray | None = None,
+                 bias: np.ndarray | None = None, nthreads: int = 1, images: tuple | None = None):
+    """The RI layer on the reference's own code path: R x tiled_scatter_conv per image
+    (ref_ri_slices) + the SPEC pooling and bias.  Same shapes as ri_forward (float32)."""
+    x = np.ascontiguousarray(x, np.float32)
+    w0 = np.ascontiguousarray(w0, np.float32)
+    src = np.ascontiguousarray(build_bases(d, w0, w1 if w1 is not None else w0), np.float32) \
+        if d.group == "steer" else w0
+    ro = d.out_orientations
+    y = np.zeros((d.n, d.c_out, ro, d.h, d.w), np.float32)
+    a = np.zeros((d.n, d.c_out, ro, d.h, d.w), np.uint8) if d.has_argmax else None
+    b = np.ascontiguousarray(bias, np.float32) if bias is not None else None
+    b0, b1 = images if images is not None else (0, d.n)
+    ref().ref_ri_batch_f(GROUPS[d.group], d.orientations, CONVENTIONS[d.convention], POOLS[d.pool],
+                         d.pool_group, _p(x), d.n, d.c_in, d.h, d.w, _p(src), d.c_out, d.k,
+                         _p(b) if b is not None else None, _p(y), _p(a) if a is not None else None,
+                         nthreads, b0, b1)
+    if d.pool in ("avg", "max"):
+        y = y[:, :, 0]
+        a = a[:, :, 0] if a is not None else None
+    return y, a
+
+
 def ref_tiled_batch(x: np.ndarray, w: np.ndarray, nthreads: int, images: tuple):
     x, w = np.ascontiguousarray(x, np.float32), np.ascontiguousarray(w, np.float32)
     n, c, h, ww = x.shape

@@ -202,6 +202,58 @@ int ref_tiled_batch_f(const float* x, int n, int c, int h, int w, const float* w
   return 0;
 }
 
+// The whole RI layer on a batch from the reference's own code path (the CPU baseline and
+// reference arm of bench.py for R > 1): for every image the R orientation slices as
+// R x tiled_scatter_conv (ri_slices above: the reference has no reuse path), then the
+// SPEC orientation reduction (the reference ships no pooling) and the bias
+// (P5), with the conventions of DESIGN.md (P2 orbit-major order, P3 argmax: global for
+// max, block-local for subgroup, ties -> smallest index).  pool: 0 none, 1 avg, 2 max,
+// 3 subgroup.  Images [begin, end), one std::thread per host core, round-robin.
+int ref_ri_batch_f(int group, int orientations, int convention, int pool, int pool_group,
+                   const float* x, int n, int cin, int h, int w, const float* bases_or_w, int cout,
+                   int k, const float* bias, float* y, uint8_t* am, int nthreads, int begin,
+                   int end) {
+  if (end > n) end = n;
+  const int R = orientations;
+  const int gf = pool == 0 ? 1 : (pool == 3 ? pool_group : R);
+  const int RO = R / gf;
+  const size_t plane = (size_t)h * w, xin = (size_t)cin * plane, yout = (size_t)cout * RO * plane;
+  std::vector<std::thread> pool_threads;
+  for (int t = 0; t < nthreads; ++t)
+    pool_threads.emplace_back([&, t] {
+      std::vector<float> f((size_t)cout * R * plane);
+      for (int i = begin + t; i < end; i += nthreads) {
+        ri_slices<float>(group, R, convention, x + i * xin, cin, h, w, bases_or_w, cout, k, f.data());
+        float* yi = y + i * yout;
+        uint8_t* ai = am ? am + i * yout : nullptr;
+        for (int co = 0; co < cout; ++co) {
+          const float bz = bias ? bias[co] : 0.f;
+          for (int s = 0; s < RO; ++s)
+            for (size_t p = 0; p < plane; ++p) {
+              const float* fs = f.data() + ((size_t)co * R + (size_t)s * gf) * plane + p;
+              float v = fs[0];
+              int arg = 0;
+              if (pool == 1) {
+                for (int r = 1; r < R; ++r) v += fs[(size_t)r * plane];
+                v = v / (float)R;
+              } else {
+                for (int r = 1; r < gf; ++r)
+                  if (fs[(size_t)r * plane] > v) {
+                    v = fs[(size_t)r * plane];
+                    arg = r;
+                  }
+              }
+              const size_t o = ((size_t)co * RO + s) * plane + p;
+              yi[o] = v + bz;
+              if (ai) ai[o] = (uint8_t)arg;
+            }
+        }
+      }
+    });
+  for (auto& th : pool_threads) th.join();
+  return 0;
+}
+
 void ref_pack_cnhw_f(const float* batch, int n, int c, int h, int w, float* out) {
   std::vector<R::Tensor3<float>> ts;
   for (int i = 0; i < n; ++i) ts.push_back(t3(batch + (size_t)i * c * h * w, c, h, w));

@@ -40,3 +40,29 @@ def test_clock_sampler_unsampled_summary():
     c.rows.append((1965.0, 1965.0, ["Not Active", "Not Active", "Not Active", "Active"]))
     s = c.summary()
     assert s["sm_mhz"] == 1965.0 and s["reasons"] == ["sw_power_cap"] and s["samples"] == 1
+
+
+def test_reference_arm_runs_the_reference_code_on_a_sample():
+    """cpu_reference: kind "reference" = R x the unmodified tiled_scatter_conv (oracle/_ref),
+    kind "port" = the oracle's reuse loop; both report the sample they timed."""
+    import bench
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import oracle as O
+    wl = (6, 8, 8, 8, 16, 3, "steer", 8, "subgroup", 4, "tiny")
+    v, info = bench.cpu_reference(wl, 2, target_s=0.0, kind="reference")
+    assert v > 0 and info["images"] == 2 and info["cores"] == 2
+    assert info["kind"] == ("reference" if O.ref_available() else "port")
+    vp, ip = bench.cpu_reference(wl, 2, target_s=0.0, kind="port", m0=3)
+    assert vp > 0 and ip["kind"] == "port" and ip["images"] == 3
+
+
+def test_both_arms_quote_the_same_config():
+    import argparse
+    import bench
+    for name in ("c1", "c3", "c4"):
+        args = argparse.Namespace(workload=name, gpus=2)
+        c = bench.workload_config(args, bench.WORKLOADS[name], 2)
+        assert c == bench.workload_config(args, bench.WORKLOADS[name], 2)
+        assert "kernel" not in c and "precision" not in c
+    c4 = bench.workload_config(argparse.Namespace(workload="c4", gpus=8), bench.WORKLOADS["c4"], 8)
+    assert c4["global_batch"] == 512 and c4["n_per_gpu"] == 64

@@ -114,3 +114,25 @@ def test_batch_forward_threads_invariant(O):
     y1, a1 = O.ri_forward(d, x, fx, fy, nthreads=1)
     y4, a4 = O.ri_forward(d, x, fx, fy, nthreads=4)
     assert np.array_equal(y1, y4) and np.array_equal(a1, a4)
+
+
+@pytest.mark.parametrize("group,R,pool,g", [("p4", 4, "max", 4), ("p4m", 8, "subgroup", 4), ("steer", 8, "subgroup", 4),
+                                            ("steer", 16, "subgroup", 8), ("p4m", 8, "avg", 4), ("p4", 4, "none", 4),
+                                            ("single", 1, "none", 1)])
+def test_reference_built_layer_equals_oracle_layer(O, group, R, pool, g):
+    """bench.py's reference arm: the layer built from the reference's own code path (R x
+    tiled_scatter_conv per image, ref_ri_batch) equals the oracle's fused reuse layer
+    (ri_forward) bit-for-bit -- values, argmax, bias -- over a multi-image batch."""
+    _need_ref(O)
+    rng = np.random.default_rng(R + len(pool))
+    n, cin, h, w, co = 3, 5, 7, 6, 4
+    d = O.Desc(n, cin, h, w, co, 3, group, R, pool, g)
+    x = rng.standard_normal((n, cin, h, w)).astype(np.float32)
+    w0 = rng.standard_normal((co, cin, 3, 3)).astype(np.float32)
+    w1 = rng.standard_normal((co, cin, 3, 3)).astype(np.float32)
+    b = rng.standard_normal(co).astype(np.float32)
+    y_ref, a_ref = O.ref_ri_batch(d, x, w0, w1, b, nthreads=2)
+    y, a = O.ri_forward(d, x, w0, w1, b)
+    assert np.array_equal(y_ref, y), np.abs(y_ref - y).max()
+    if a is not None:
+        assert np.array_equal(a_ref, a)

@@ -8,7 +8,7 @@ for w in ${WL:-c3 c4}; do
 import json
 d=json.loads(open("gpurun_out/bench_${w}_${pr}.json").read().strip().splitlines()[-1])
 r=d["roofline"]
-print("$w $pr", d["config"].get("kernel"), "step_ms", round(d["ms_per_step"],4), "kernel_ms", round(r["kernel_ms"],4), "frac", round(r["frac"],4), d.get("clocks"))
+print("$w $pr", d.get("kernel"), "step_ms", round(d["ms_per_step"],4), "kernel_ms", round(r["kernel_ms"],4), "frac", round(r["frac"],4), d.get("clocks"))
 PY
   done
 done
