@@ -94,6 +94,24 @@ constexpr int MAX_NC = 8;                // ci chunks of 64 (Cin <= 512)
 constexpr int MAX_STAGES = 8;
 constexpr int XH = 16;                   // output columns per epilogue thread
 
+// In-kernel cycle accounting for experiments (tools/tc_kernel_profile.py builds a variant of
+// the library with -DRC_TC_PROF=1; the shipped build compiles it out).  Per CTA, 16 counters:
+//   MMA warp w (w = 0, 1) at 5w: total, wait D buffer, wait X band, wait W stage, issue
+//   10 epilogue warp 4: total, 11 wait D full, 12 finalize; 13 producer 0 wait W slot,
+//   14 producer 0 wait X slot, 15 producer 1 wait W slot
+#ifndef RC_TC_PROF
+#define RC_TC_PROF 0
+#endif
+#if RC_TC_PROF
+__device__ unsigned long long g_tc_prof[1024 * 16];
+#define PROF_T(v) const long long v = clock64()
+#define PROF_ADD(slot, t0) \
+  if ((threadIdx.x & 31) == 0) atomicAdd(&g_tc_prof[blockIdx.x * 16 + (slot)], (unsigned long long)(clock64() - (t0)))
+#else
+#define PROF_T(v)
+#define PROF_ADD(slot, t0)
+#endif
+
 // Input rows [first, end) of full-row band k (band rows 0 .. IN_ROWS-1 = image rows
 // OUT_ROWS*k - 1 ...) that lie inside the image; the others are the zero padding.
 template <int TW>
@@ -357,7 +375,9 @@ __device__ __forceinline__ void epi_tap(EpiState& e, float (&Y)[RPB][XH], uint64
   constexpr int NDB = Geo<TW>::NDB;
   const uint32_t a = e.row_base + e.db * Geo<TW>::DCOLS;
   float z[18];
+  PROF_T(t_df);
   mbar_wait(&d_full[e.db], e.dph);
+  if (threadIdx.x / 32 == EPI_WARP0) PROF_ADD(11, t_df);
   tc_fence_after();
   if constexpr (Geo<TW>::SMALL) {
     constexpr int TR = Geo<TW>::TR;
@@ -413,6 +433,7 @@ __device__ void epilogue(const TcParams& p, uint32_t tmem, uint64_t* d_full, uin
                                                                            // writes the same zeros
   const int nstrip = G::STRIP ? p.W / 16 : 1;
   float Y[RPB][XH];
+  PROF_T(t_epi0);
   for (int item = blockIdx.x; item < p.items; item += gridDim.x) {
     const int n = item / p.NCT, ct = item % p.NCT;
     const int co = ct * 128 + co_l;
@@ -440,9 +461,12 @@ __device__ void epilogue(const TcParams& p, uint32_t tmem, uint64_t* d_full, uin
         const int row = G::SMALL ? o0 : G::OUT_ROWS * (k / nstrip) + srow;
         const int x0 = G::SMALL ? 0 : (k % nstrip) * 16;
         const int img = G::SMALL ? n * G::IMGS + s_img : n;  // small: n indexes bands of IMGS images
+        PROF_T(t_fin);
         if (img < p.N && co < p.Cout && row < p.H) finalize_row<TW, RPB>(p, Y, img, co, b, row, x0);
+        if (warp == EPI_WARP0) PROF_ADD(12, t_fin);
       }
   }
+  if (warp == EPI_WARP0) PROF_ADD(10, t_epi0);
 }
 
 // smem ring position: stage index + phase parity, advanced without division
@@ -520,7 +544,9 @@ __global__ void __launch_bounds__(THREADS, 1) ri_tc_kernel(const __grid_constant
         const size_t tile = ((size_t)n * p.NBK + k) * p.NC;
         if (me == 0 && !p.xstream) {  // new band: its X chunks (both MMA warps read them)
           for (int c = 0; c < p.NC; ++c) {
+            PROF_T(t_xe);
             if (xc > 0) mbar_wait(&x_empty[c], (xc - 1) & 1);
+            PROF_ADD(14, t_xe);
             if (elect_one()) {
               mbar_arrive_expect_tx(&x_full[c], parts * XS);
               bulk_g2s(xs + c * XS, p.xh + (tile + c) * XS, XS, &x_full[c]);
@@ -535,7 +561,9 @@ __global__ void __launch_bounds__(THREADS, 1) ri_tc_kernel(const __grid_constant
             if ((gd & 1u) != me) continue;
             for (int sp = 0; sp < stages_per_tap; ++sp) {
               const int st = t * stages_per_tap + sp;
+              PROF_T(t_we);
               if (wr.used) mbar_wait(&w_empty[base + wr.s], wr.ph ^ 1);
+              PROF_ADD(me == 0 ? 13 : 15, t_we);
               if (elect_one()) {
                 uint64_t* full = &w_full[base + wr.s];
                 mbar_arrive_expect_tx(full, stage_bytes);
@@ -572,6 +600,7 @@ __global__ void __launch_bounds__(THREADS, 1) ri_tc_kernel(const __grid_constant
     uint32_t xc = 0, gd = 0;  // gd: global tap index
     int db = 0;
     uint32_t dph = 0;
+    PROF_T(t_mma0);
     for (int item = blockIdx.x; item < p.items; item += gridDim.x) {
       for (int k = 0; k < p.NBK; ++k) {
         // full-row bands at the image top / bottom: the halo rows outside the image are zero
@@ -591,14 +620,21 @@ __global__ void __launch_bounds__(THREADS, 1) ri_tc_kernel(const __grid_constant
             const bool first_mine = tb < 2;                 // this warp's first tap of the band
             const bool last_mine = tb + 2 >= taps_per_band;  // ... and its last one
             if (mine) {
+              PROF_T(t_d);
               if (gd >= (uint32_t)NDB) mbar_wait(&d_empty[db], dph ^ 1);
+              PROF_ADD(5 * me + 1, t_d);
               tc_fence_after();
               const uint32_t d = tmem + G::D0 + db * G::DCOLS + doff_k;
               for (int sp = 0; sp < stages_per_tap; ++sp) {
+                PROF_T(t_x);
                 if (first_mine && !p.xstream)
                   for (int cl = 0; cl < p.spc; ++cl) mbar_wait(&x_full[sp * p.spc + cl], xc & 1);
+                PROF_ADD(5 * me + 2, t_x);
+                PROF_T(t_w);
                 mbar_wait(&w_full[base + wr.s], wr.ph);
+                PROF_ADD(5 * me + 3, t_w);
                 tc_fence_after();
+                PROF_T(t_i);
                 if (elect_one()) {
                   const uint32_t wbase = smem_u32(ws + (base + wr.s) * stage_bytes);
                   // descriptors are linear in the smem address (14-bit field, smem < 256 KB): one
@@ -627,6 +663,7 @@ __global__ void __launch_bounds__(THREADS, 1) ri_tc_kernel(const __grid_constant
                   if (sp == stages_per_tap - 1) mma_commit(&d_full[db]);
                 }
                 __syncwarp();
+                PROF_ADD(5 * me + 4, t_i);
                 wr.adv(S_me);
               }
             }
@@ -640,6 +677,7 @@ __global__ void __launch_bounds__(THREADS, 1) ri_tc_kernel(const __grid_constant
         }
       }
     }
+    PROF_ADD(5 * me, t_mma0);
   } else if (warp >= EPI_WARP0) {
     // ------------------------------------------------------------ epilogue
     asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(REGS_EPILOGUE));
@@ -926,5 +964,16 @@ int launch_tc(const rc_desc& d, const float* x, const void* bank, const float* b
   RC_CUDA(cudaGetLastError());
   return RC_OK;
 }
+
+#if RC_TC_PROF
+extern "C" int rc_tc_prof(unsigned long long* host, int n, int reset) {
+  if (host && n > 0) RC_CUDA(cudaMemcpyFromSymbol(host, g_tc_prof, sizeof(unsigned long long) * (size_t)n));
+  if (reset) {
+    static unsigned long long zeros[1024 * 16];
+    RC_CUDA(cudaMemcpyToSymbol(g_tc_prof, zeros, sizeof(zeros)));
+  }
+  return RC_OK;
+}
+#endif
 
 }  // namespace rc

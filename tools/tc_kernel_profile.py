@@ -1,0 +1,82 @@
+"""In-kernel cycle accounting of the band kernel (ri_tc.cu, RC_TC_PROF counters).
+
+Builds a profiling variant of the library (ri_tc.cu with -DRC_TC_PROF=1, the other objects
+from the normal build) into tools/variants/, runs one layer config a few times and prints,
+per CTA on average: each MMA warp's total / waiting-for-D / waiting-for-X / waiting-for-W /
+issuing cycles, the epilogue warp's total / waiting-for-D / finalize cycles and the
+producers' waits.  Experiment tooling; the shipped library has the counters compiled out.
+
+    python tools/tc_kernel_profile.py build            # here (nvcc cross-compiles)
+    python tools/tc_kernel_profile.py run N CIN H W COUT GROUP R POOL G [precision]
+"""
+import ctypes as C
+import os
+import subprocess
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+VAR = os.path.join(ROOT, "tools", "variants")
+LIB = os.path.join(VAR, "librotconv_prof.so")
+NAMES = ["mma0 total", "mma0 wait D", "mma0 wait X", "mma0 wait W", "mma0 issue",
+         "mma1 total", "mma1 wait D", "mma1 wait X", "mma1 wait W", "mma1 issue",
+         "epi total", "epi wait Dfull", "epi finalize", "prod0 wait Wslot", "prod0 wait Xslot",
+         "prod1 wait Wslot"]
+
+
+def build():
+    from paper_2512_08888_b200 import build as B
+    B.build()
+    os.makedirs(VAR, exist_ok=True)
+    obj = os.path.join(VAR, "ri_tc_prof.o")
+    subprocess.check_call([B.NVCC, *B.ARCH, *[f for f in B.FLAGS if f not in ("-Xptxas", "-v")],
+                           "-DRC_TC_PROF=1", "-c", os.path.join(B.CSRC, "ri_tc.cu"), "-o", obj])
+    objs = [os.path.join(B.BUILD, f) for f in sorted(os.listdir(B.BUILD))
+            if f.endswith(".o") and f != "ri_tc.o"] + [obj]
+    subprocess.check_call([B.NVCC, *B.ARCH, "-shared", "-o", LIB, *objs, "-lcublas"])
+    print(LIB)
+
+
+def run(a):
+    import torch
+    from paper_2512_08888_b200 import _lib
+    _lib.LIB_PATH = LIB
+    _lib.SIGNATURES["rc_tc_prof"] = (C.c_int, [C.c_void_p, C.c_int, C.c_int])
+    import paper_2512_08888_b200 as P
+    n, cin, h, w, cout = map(int, a[:5])
+    group, R, pool, g = a[5], int(a[6]), a[7], int(a[8])
+    prec = a[9] if len(a) > 9 else "auto"
+    desc = P.Desc(n, cin, h, w, cout, 3, group, R, pool, g, "scatter", prec)
+    x = torch.rand((n, cin, h, w), device="cuda") * 2 - 1
+    w0 = (torch.rand((cout, cin, 3, 3), device="cuda") * 2 - 1) * 0.05
+    w1 = (torch.rand((cout, cin, 3, 3), device="cuda") * 2 - 1) * 0.05 if group == "steer" else None
+    bank = P.bank_precompute(desc, w0, w1)
+    L = _lib.lib()
+    reps = 5
+    for _ in range(2):
+        P.ri_conv_forward(desc, x, bank)
+    torch.cuda.synchronize()
+    L.rc_tc_prof(None, 0, 1)
+    a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a0.record()
+    for _ in range(reps):
+        P.ri_conv_forward(desc, x, bank)
+    a1.record()
+    torch.cuda.synchronize()
+    buf = (C.c_ulonglong * (1024 * 16))()
+    L.rc_tc_prof(buf, 1024 * 16, 0)
+    sms = torch.cuda.get_device_properties(0).multi_processor_count
+    ctas = min(sms, (cout + 127) // 128 * n)
+    tot = [sum(buf[c * 16 + i] for c in range(ctas)) / ctas / reps for i in range(16)]
+    ms = a0.elapsed_time(a1) / reps
+    print(f"{desc.kernel_name()} {ms:.3f} ms per launch (incl. x_pack), {ctas} CTAs; per CTA per launch, "
+          f"Mcycles (share of the MMA warp 0 total):")
+    for i, nm in enumerate(NAMES):
+        print(f"  {nm:18s} {tot[i] / 1e6:8.3f}  {tot[i] / max(tot[0], 1):6.3f}")
+
+
+if __name__ == "__main__":
+    if sys.argv[1] == "build":
+        build()
+    else:
+        run(sys.argv[2:])
