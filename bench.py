@@ -401,6 +401,7 @@ def run_stack(args, wl):
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
         dist.init_process_group("nccl", device_id=dev)
     n_total = wl[0]
     b, e = P.shard_range(n_total, world, rank)
@@ -429,8 +430,11 @@ def run_stack(args, wl):
         dist.barrier()
     times = [a.elapsed_time(bb) for a, bb in ev]
     tot = torch.tensor([sum(times)], dtype=torch.float64, device=dev)
+    per_rank = [tot.clone() for _ in range(world)]
     if world > 1:
+        dist.all_gather(per_rank, tot)
         dist.all_reduce(tot, op=dist.ReduceOp.MAX)
+    per_rank_ms = [round(t.item() / args.steps, 4) for t in per_rank]
     ms = tot.item() / args.steps
     eff_total = stack.eff_flops(n_total)
     value = eff_total / (ms * 1e-3) / 1e12
@@ -487,7 +491,7 @@ def run_stack(args, wl):
             "config": stack_config(args, wl, world),
             "precision": args.precision, "kernels": stack.kernels(n), "cuda_graph": True,
             "l2": "flushed between timed iterations (512 MB write)",
-            "alg_tflops": stack.alg_flops(n_total) / (ms * 1e-3) / 1e12,
+            "alg_tflops": stack.alg_flops(n_total) / (ms * 1e-3) / 1e12, "per_rank_ms": per_rank_ms,
             "layer_ms": [round(t, 4) for t, _ in layer_ms],
             "roofline": {"bound": "tensor" if top.kernel_name().startswith("tc_") else "fp32-simt",
                          "kernel": top.kernel_name(), "achieved": achieved,
@@ -540,6 +544,7 @@ def main():
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
+        os.environ.setdefault("NCCL_DEBUG", "INFO")  # communicator lines on stderr (rank check)
         dist.init_process_group("nccl", device_id=dev)
     n, cin, h, w, cout, k, g, R, pool, pg, label = wl
     strong = args.workload in STRONG
@@ -592,8 +597,11 @@ def main():
     torch.cuda.synchronize()
     times = [a.elapsed_time(b) for a, b in ev]  # ms, on the launching stream
     tot = torch.tensor([sum(times)], dtype=torch.float64, device=dev)
+    per_rank = [tot.clone() for _ in range(world)]
     if world > 1:
+        dist.all_gather(per_rank, tot)
         dist.all_reduce(tot, op=dist.ReduceOp.MAX)
+    per_rank_ms = [round(t.item() / args.steps, 4) for t in per_rank]
     ms = tot.item() / args.steps
     eff_total = 2 * n_global * h * w * k * k * cin * cout * R  # all ranks' images
     value = eff_total / (ms * 1e-3) / 1e12
@@ -661,6 +669,7 @@ def main():
             "precision": args.precision, "kernel": desc.kernel_name(),
             "l2": "flushed between timed iterations (512 MB write)",
             "alg_tflops": achieved * 1.0, "eff_tflops_per_gpu": value / world,
+            "per_rank_ms": per_rank_ms, "timing": "max over ranks of each rank's CUDA-event step time",
             "roofline": {"bound": "tensor" if tc else "fp32-simt", "kernel": desc.kernel_name(),
                          "achieved": achieved, "peak": tpeak if tc else 74.4, "unit": "TFLOP/s",
                          "frac": achieved / (tpeak if tc else 74.4), "traffic": traffic,

@@ -421,34 +421,54 @@ int rc_ri_conv_forward_host(const rc_desc* d, const float* h_x, const float* h_w
   if (dw1) RC_CUDA(cudaMemcpyAsync(dw1, h_w1, wb, cudaMemcpyHostToDevice, s));
   if (dbias) RC_CUDA(cudaMemcpyAsync(dbias, h_bias, d->c_out * sizeof(float), cudaMemcpyHostToDevice, s));
   int st = launch_bank(*d, (const float*)dw0, (const float*)dw1, dbank, s);
-  if (st != RC_OK) return st;
+  if (st != RC_OK) {
+    cudaStreamSynchronize(s);  // the queued weight uploads read the caller's buffers
+    return st;
+  }
   // Chunked pipeline over images: H2D of chunk i+1 and D2H of chunk i-1 overlap the kernels
   // of chunk i (three streams, the copies on the two copy engines).  Chunks of >= 16 images
   // keep every copy large; small batches run as one chunk.
   const int chunks = d->n >= 64 ? 8 : (d->n >= 32 ? 4 : 1);
   st = c.ensure_pipeline(2 * (size_t)chunks);
-  if (st != RC_OK) return st;
+  if (st != RC_OK) {
+    cudaStreamSynchronize(s);  // the bank upload / precompute may still read the caller's weights
+    return st;
+  }
+  // every exit after the pipeline starts drains all three streams first: queued async copies
+  // must not touch the caller's host buffers after this call has returned (even with an error)
+  auto drain = [&](int status) {
+    cudaStreamSynchronize(c.h2d);
+    cudaStreamSynchronize(s);
+    cudaStreamSynchronize(c.d2h);
+    return status;
+  };
+#define RC_PIPE(call)                                          \
+  do {                                                         \
+    cudaError_t e_ = (call);                                   \
+    if (e_ != cudaSuccess) return drain(cuda_fail(e_, #call)); \
+  } while (0)
   const size_t xi = xb / d->n, yi = yb / d->n, ai = ab / d->n;
   for (int k = 0; k < chunks; ++k) {
     int b = 0, e = 0;
     rc_shard_range(d->n, chunks, k, &b, &e);
     if (e == b) continue;
     cudaEvent_t in_ready = c.ev[2 * k], out_ready = c.ev[2 * k + 1];
-    RC_CUDA(cudaMemcpyAsync((char*)dx + b * xi, (const char*)h_x + b * xi, (e - b) * xi, cudaMemcpyHostToDevice,
+    RC_PIPE(cudaMemcpyAsync((char*)dx + b * xi, (const char*)h_x + b * xi, (e - b) * xi, cudaMemcpyHostToDevice,
                             c.h2d));
-    RC_CUDA(cudaEventRecord(in_ready, c.h2d));
-    RC_CUDA(cudaStreamWaitEvent(s, in_ready, 0));
+    RC_PIPE(cudaEventRecord(in_ready, c.h2d));
+    RC_PIPE(cudaStreamWaitEvent(s, in_ready, 0));
     rc_desc cd = *d;
     cd.n = e - b;
     st = dispatch(cd, (const float*)((char*)dx + b * xi), dbank, (const float*)dbias, (float*)((char*)dy + b * yi),
                   da ? (uint8_t*)da + b * ai : nullptr, dws, wsb, s, false, nullptr);
-    if (st != RC_OK) return st;
-    RC_CUDA(cudaEventRecord(out_ready, s));
-    RC_CUDA(cudaStreamWaitEvent(c.d2h, out_ready, 0));
-    RC_CUDA(cudaMemcpyAsync((char*)h_y + b * yi, (char*)dy + b * yi, (e - b) * yi, cudaMemcpyDeviceToHost, c.d2h));
+    if (st != RC_OK) return drain(st);
+    RC_PIPE(cudaEventRecord(out_ready, s));
+    RC_PIPE(cudaStreamWaitEvent(c.d2h, out_ready, 0));
+    RC_PIPE(cudaMemcpyAsync((char*)h_y + b * yi, (char*)dy + b * yi, (e - b) * yi, cudaMemcpyDeviceToHost, c.d2h));
     if (has_arg)
-      RC_CUDA(cudaMemcpyAsync(h_argmax + b * ai, (uint8_t*)da + b * ai, (e - b) * ai, cudaMemcpyDeviceToHost, c.d2h));
+      RC_PIPE(cudaMemcpyAsync(h_argmax + b * ai, (uint8_t*)da + b * ai, (e - b) * ai, cudaMemcpyDeviceToHost, c.d2h));
   }
+#undef RC_PIPE
   RC_CUDA(cudaStreamSynchronize(c.d2h));
   RC_CUDA(cudaStreamSynchronize(s));
   return RC_OK;
@@ -476,7 +496,10 @@ int rc_steer_host(const float* h_fx, const float* h_fy, size_t count, double the
   RC_CUDA(cudaMemcpyAsync(dx, h_fx, b, cudaMemcpyHostToDevice, s));
   RC_CUDA(cudaMemcpyAsync(dy, h_fy, b, cudaMemcpyHostToDevice, s));
   int st = launch_steer((const float*)dx, (const float*)dy, count, theta, (float*)dout, s);
-  if (st != RC_OK) return st;
+  if (st != RC_OK) {  // drain the queued copies of the caller's host buffers first
+    cudaStreamSynchronize(s);
+    return st;
+  }
   RC_CUDA(cudaMemcpyAsync(h_out, dout, b, cudaMemcpyDeviceToHost, s));
   RC_CUDA(cudaStreamSynchronize(s));
   return RC_OK;
@@ -504,9 +527,15 @@ int rc_orientation_bank_host(const rc_desc* d, const float* h_w0, const float* h
   RC_CUDA(cudaMemcpyAsync(dw0, h_w0, wb, cudaMemcpyHostToDevice, s));
   if (dw1) RC_CUDA(cudaMemcpyAsync(dw1, h_w1, wb, cudaMemcpyHostToDevice, s));
   int st = launch_bank(*d, (const float*)dw0, (const float*)dw1, dbank, s);
-  if (st != RC_OK) return st;
+  if (st != RC_OK) {  // drain the queued copies of the caller's host buffers first
+    cudaStreamSynchronize(s);
+    return st;
+  }
   st = launch_orientation_bank(*d, dbank, (float*)dk, s);
-  if (st != RC_OK) return st;
+  if (st != RC_OK) {  // drain the queued copies of the caller's host buffers first
+    cudaStreamSynchronize(s);
+    return st;
+  }
   RC_CUDA(cudaMemcpyAsync(h_kernels, dk, kb, cudaMemcpyDeviceToHost, s));
   RC_CUDA(cudaStreamSynchronize(s));
   return RC_OK;
@@ -542,7 +571,10 @@ int rc_orientation_pool_host(int n, int c_out, int r, int h, int w, int pool, in
   if (dbias) RC_CUDA(cudaMemcpyAsync(dbias, h_bias, c_out * sizeof(float), cudaMemcpyHostToDevice, s));
   int st = launch_pool(n, c_out, r, h, w, pool, pool_group, (const float*)df, (const float*)dbias, (float*)dy,
                        (uint8_t*)da, s);
-  if (st != RC_OK) return st;
+  if (st != RC_OK) {  // drain the queued copies of the caller's host buffers first
+    cudaStreamSynchronize(s);
+    return st;
+  }
   RC_CUDA(cudaMemcpyAsync(h_y, dy, yb, cudaMemcpyDeviceToHost, s));
   if (has_arg) RC_CUDA(cudaMemcpyAsync(h_argmax, da, yb / sizeof(float), cudaMemcpyDeviceToHost, s));
   RC_CUDA(cudaStreamSynchronize(s));
