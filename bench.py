@@ -250,28 +250,31 @@ def run_reference(args, wl):
 
 
 def smem_traffic(desc, kernel: str):
-    """Shared-memory bytes one launch of the band kernel (ri_tc.cu) moves, from its geometry:
-    per K-step (16 ci of one chunk) the SS MMAs read A = passes_A x 4 KB of weights and
-    B = passes_B x N x 32 B of the X band (bf16x3: Ah twice + Al once, Xh twice + Xl once),
-    and the TMA writes parts x 4 KB of weights; plus the X band writes.  None for other kernels."""
+    """Shared-memory bytes one launch of the band kernel (ri_tc.cu) moves, from its geometry;
+    None for other kernels.  Per K-step (16 ci of one chunk):
+      * 16-wide carry bands (tc_k3w16; N = 64 px, no halo): bf16x3 reads A = Wh once (the
+        N = 128 Wh x [Xh | Xl] MMA) + Wl once (Wl x Xh) and B = 128 + 64 rows x 32 B; bf16
+        reads A once and B = 64 rows; the TMA writes parts x 4 KB of weights.  The X band
+        (parts x NC x 64 px x 128 B) is written once per (base, band) unit.
+      * strips (tc_k3strip; 6x18 input px, N = 112): bf16x3 reads Ah twice + Al once and
+        Xh twice + Xl once; X written once per band (shared by the bases)."""
     if not (kernel.startswith("tc_k3w16") or kernel.startswith("tc_k3strip")):
         return None
     three = kernel.endswith("bf16x3")
-    parts, pa = (2, 3) if three else (1, 1)
+    parts = 2 if three else 1
     n, h, w, cin, cout = desc.n, desc.h, desc.w, desc.c_in, desc.c_out
     NB = {"single": 1, "p4": 1, "p4m": 2, "steer": desc.orientations // 4}[desc.group]
     NC = (cin + 63) // 64
     NCT = (cout + 127) // 128
-    if kernel.startswith("tc_k3w16"):  # bands of 4 rows; full-row bands skip out-of-image halo rows
-        bands = []
-        for k in range((h + 3) // 4):
-            r0 = 4 * k - 1
-            lo, hi = (1 if r0 < 0 else 0), min(6, h - r0)
-            bands.append((hi - lo) * 16)
-    else:  # 4x16 strips of 6x18 input px, N = 112
-        bands = [112] * (((h + 3) // 4) * (w // 16))
-    kstep = lambda N: pa * 4096 + pa * N * 32 + parts * 4096
-    per_item = sum(NB * 9 * NC * 4 * kstep(N) + parts * NC * N * 128 for N in bands)
+    if kernel.startswith("tc_k3w16"):
+        nbk = (h + 3) // 4
+        kstep = (2 * 4096 + (128 + 64) * 32 + 2 * 4096) if three else (4096 + 64 * 32 + 4096)
+        per_item = NB * nbk * (9 * NC * 4 * kstep + parts * NC * 64 * 128)
+    else:
+        pa = 3 if three else 1
+        bands = ((h + 3) // 4) * (w // 16)
+        kstep = pa * 4096 + pa * 112 * 32 + parts * 4096
+        per_item = bands * (NB * 9 * NC * 4 * kstep + parts * NC * 112 * 128)
     return per_item * n * NCT
 
 

@@ -8,10 +8,18 @@
 // precision "bf16"  : one product, bf16 operands;
 // precision "bf16x3": operands split hi + lo (bf16 each); hi*hi + hi*lo + lo*hi, FP32-class.
 //
-// Work item = (co tile of 128, image); per base b the image is swept in bands of 64 output
-// pixels.  A 16-wide band is 4 output rows computed from the 6 input rows [4k-1, 4k+5) (the
-// halo rows are recomputed: no cross-band state in TMEM and no cross-warp races); bands at
-// the image top / bottom skip the halo rows outside the image.
+// Work item = (co tile of 128, image); the image is swept in bands of 64 output pixels.
+//
+// 16-wide images (the C3 shape): a band is 4 input rows [4k, 4k+4) and NO halo rows.  The
+// MMA computes Z for exactly the band's input pixels; output rows that also depend on the
+// neighbouring bands are carried across bands in TMEM: band k completes output rows
+// [4k-1, 4k+3); the partial sums of row 4k+3 (input rows 4k+2, 4k+3) and of row 4k+4
+// (input row 4k+3) are kept for band k+1.  Bases are the outer loop (the carry is per base).
+// bf16x3 runs two MMAs per K-step: Wh x [Xh | Xl] (N = 128, one read of the hi weight tile
+// for two products) and Wl x Xh (N = 64, accumulating into the first half); the epilogue
+// sums the two halves.  Per K-step the shared-memory port then carries 8 KB of weight
+// writes + 8 KB of A reads + 6 KB of B reads (was 8 + 12 + 8.25 with 6-row halo bands).
+// Other widths (strips of 4x16, whole 8x8 / 4x4 images) keep halo bands (below).
 //
 // Persistent CTA (1 per SM), 20 warps:
 //   warps 1, 2  MMA       : two issuers, alternating taps (warp 1 the even, warp 2 the odd taps
@@ -30,10 +38,10 @@
 //                           completed (the parity of phase n+1 is that of phase n-1).  Warp 0
 //                           also loads the X band (NC tiles of [MMA_N px x 64 ci]).
 //   warps 4-19  epilogue  : TMEM lane = output channel co.  The 4 warps of a lane quadrant
-//                           own the band's 4 output rows (one each); a thread holds
-//                           Y[4 rotations][16 px] = 64 fp32 registers, pulls the 3 input rows
-//                           it needs from TMEM (one 16-column load each), scatters with
-//                           compile-time offsets (taps unrolled), then pools + stores.
+//                           own 4 output rows of the band (16-wide: roles, see epi_tap_carry);
+//                           a thread holds Y[4 rotations][16 px] = 64 fp32 registers, pulls the
+//                           input rows it needs from TMEM (one 16-column load each), scatters
+//                           with compile-time offsets (taps unrolled), then pools + stores.
 // Pooling / argmax / bias epilogue identical to the SIMT kernel; 128-bit stores.
 #include <cuda_bf16.h>
 
@@ -49,76 +57,91 @@ namespace {
 using namespace tc;
 
 // Band geometry.  A band is 64 output pixels (the register budget of the epilogue: every
-// epilogue thread owns 16 of them) computed from the input rows/columns they depend on:
-//   TW = 16 : 4 full rows of a 16-wide image from 6 input rows           (N = 96)
+// epilogue thread owns 16 of them):
+//   TW = 16 : CARRY -- 4 full rows of a 16-wide image, input rows = output rows, the
+//             rows that need the neighbouring bands are carried in TMEM (N = 64; 128 for
+//             the bf16x3 [Xh | Xl] concatenation)
 //   TW = 0  : strip of 4 rows x 16 columns of a wider image (W % 16 == 0, W >= 32) from
-//             6 input rows x 18 columns incl. the halo columns           (N = 112, 108 used)
+//             6 input rows x 18 columns incl. the halo                  (N = 112, 108 used)
 //   TW = 8, 4 (H == W): small images, whole images per band and no halo rows at all (the
 //             window rows outside an image are the zero padding): 1 image of 8x8 or 4
 //             images of 4x4 per band (N = 64); a thread owns TR = 16/W full rows.
 // RS is the TMEM / operand row stride (pixels per input row of the band).
 // (Measured and rejected in round 1, not shipped: 2-row bands for W = 32, CTA pairs, the hi
-// weight tile staged in TMEM, N = 192 hi/lo concatenation -- DESIGN.md 3.1.)
+// weight tile staged in TMEM -- DESIGN.md 3.1.)
+#ifndef RC_TC_ABLATE_W  // experiment switches (compile time, profiling builds only)
+#define RC_TC_ABLATE_W 0
+#endif
+#ifndef RC_TC_ABLATE_X
+#define RC_TC_ABLATE_X 0
+#endif
+#ifndef RC_TC_CAT  // experiment switch (compile time): 0 = CARRY bf16x3 as three N = 64 MMAs
+#define RC_TC_CAT 1
+#endif
 template <int TW>
 struct Geo {
   static constexpr bool STRIP = TW == 0;
   static constexpr bool SMALL = TW == 4 || TW == 8;
+  static constexpr bool CARRY = TW == 16;
+  static constexpr bool CAT = CARRY && RC_TC_CAT;             // bf16x3 as Wh x [Xh | Xl] + Wl x Xh
   static constexpr int OUT_ROWS = STRIP ? 4 : 64 / TW;        // 4 | 4 | 8 | 16
-  static constexpr int IN_ROWS = SMALL ? OUT_ROWS : OUT_ROWS + 2;
+  static constexpr int IN_ROWS = (SMALL || CARRY) ? OUT_ROWS : OUT_ROWS + 2;
   static constexpr int RS = STRIP ? 18 : TW;                  // pixels per band row
-  static constexpr int BAND_PX = IN_ROWS * RS;                // 96 | 108 | 64 | 64
+  static constexpr int BAND_PX = IN_ROWS * RS;                // 64 | 108 | 64 | 64
   static constexpr int MMA_N = (BAND_PX + 15) / 16 * 16;
   static constexpr int XTILE = MMA_N * 64 * 2;                // bytes of one [MMA_N x 64 ci] bf16 tile
-  // D buffers from column D0.  Columns [0, D0) keep the 1-column-left halo load of a band's
-  // first pixel inside the allocation; full-row bands also read their skipped (out-of-image)
-  // window rows from them as zeros (band_rows), so they need D0 >= 18.
-  static constexpr uint32_t D0 = (STRIP || SMALL) ? 16 : 32;
-  static constexpr int DCOLS = MMA_N;                         // TMEM columns per D buffer
-  static constexpr int NDB = DCOLS * 5 + D0 <= 512 ? 5 : (DCOLS * 4 + D0 <= 512 ? 4 : 3);
+  // TMEM: columns [0, D0) hold the carried rows (CARRY: [0, 64) row 4k-1 of the band, [64,
+  // 128) row 4k+4) or keep the 1-column-left halo load of a band's first pixel inside the
+  // allocation (strips, small images); D buffers from D0.  A CARRY D buffer is [Z of Xh |
+  // Z of Xl] (the bf16 one-pass kernel uses the first half).
+  static constexpr uint32_t D0 = CARRY ? 128 : 16;
+  static constexpr int DCOLS = CAT ? 2 * MMA_N : MMA_N;       // TMEM columns per D buffer
+  static constexpr int NDB = (512 - D0) / DCOLS < 6 ? (512 - D0) / DCOLS : 6;
   static constexpr int TR = SMALL ? 16 / TW : 1;              // output rows per epilogue thread
   static constexpr int IMGS = SMALL ? 64 / (TW * TW) : 1;     // images per band
-  static constexpr bool TRIM = !STRIP && !SMALL;              // full-row bands: see band_rows
 };
 constexpr int KC = 64;                  // ci per chunk (one 128-byte swizzle row of bf16)
 constexpr int WTILE = 128 * KC * 2;      // 16 KB
-constexpr int NUM_EPI = 16;              // epilogue warps (4 warpgroups)
 constexpr int EPI_WARP0 = 4;             // warps 0-3: producer warpgroup (TMA, 2 x MMA, idle)
 constexpr int NUM_MMA = 2;               // MMA-issuing warps (1 and 2)
-constexpr int THREADS = 32 * (EPI_WARP0 + NUM_EPI);
-constexpr int REGS_PRODUCER = 64;        // setmaxnreg budgets: 20 warps x 96 at launch; the MMA
-                                         // warp's loop spills at 32 (-2..5% with 64/104,
-                                         // profiles/r01/regsplit_ab.txt)
-constexpr int REGS_EPILOGUE = 104;
-constexpr int MAX_NDB = 5;
+// Warps and setmaxnreg budgets.  Halo bands: 16 epilogue warps (one 16-px row of 4
+// rotations each) x 104 registers, warps 0-3 at 64 (the MMA warp's loop spills at 32: -2..5%,
+// profiles/r01/regsplit_ab.txt).  CARRY bands: 8 epilogue warps x 224 (two rows each: the
+// [Xh | Xl] row sums and the carried rows need more than 112 registers per one-row thread),
+// warps 0-3 at 56.  setmaxnreg.inc only redistributes the CTA's launch allocation (THREADS x
+// the kernel's register count R0: 96 at 640 threads, 168 at 384), so 128 x PROD + 32 x WARPS
+// x REGS must not exceed THREADS x R0 -- a larger budget would block setmaxnreg.inc forever;
+// launch_tc checks it: 640 x 96 = 128 x 64 + 512 x 104;  384 x 168 = 128 x 56 + 256 x 224.
+template <int TW>
+struct Epi {
+  static constexpr int WARPS = TW == 16 ? 8 : 16;
+  static constexpr int REGS = TW == 16 ? 224 : 104;
+  static constexpr int PROD = TW == 16 ? 56 : 64;
+  static constexpr int THREADS = 32 * (EPI_WARP0 + WARPS);
+};
+constexpr int MAX_NDB = 6;
 constexpr int MAX_NC = 8;                // ci chunks of 64 (Cin <= 512)
 constexpr int MAX_STAGES = 8;
 constexpr int XH = 16;                   // output columns per epilogue thread
 
 // In-kernel cycle accounting for experiments (tools/tc_kernel_profile.py builds a variant of
-// the library with -DRC_TC_PROF=1; the shipped build compiles it out).  Per CTA, 16 counters:
+// the library with -DRC_TC_PROF=1; the shipped build compiles it out).  Per CTA, 32 slots:
 //   MMA warp w (w = 0, 1) at 5w: total, wait D buffer, wait X band, wait W stage, issue
 //   10 epilogue warp 4: total, 11 wait D full, 12 finalize; 13 producer 0 wait W slot,
-//   14 producer 0 wait X slot, 15 producer 1 wait W slot
+//   14 producer 0 wait X slot, 15 producer 1 wait W slot; 16-18 as 10-12 for epilogue
+//   warp 8 (CARRY: the second half of a lane quadrant)
 #ifndef RC_TC_PROF
 #define RC_TC_PROF 0
 #endif
 #if RC_TC_PROF
-__device__ unsigned long long g_tc_prof[1024 * 16];
+__device__ unsigned long long g_tc_prof[1024 * 32];
 #define PROF_T(v) const long long v = clock64()
 #define PROF_ADD(slot, t0) \
-  if ((threadIdx.x & 31) == 0) atomicAdd(&g_tc_prof[blockIdx.x * 16 + (slot)], (unsigned long long)(clock64() - (t0)))
+  if ((threadIdx.x & 31) == 0) atomicAdd(&g_tc_prof[blockIdx.x * 32 + (slot)], (unsigned long long)(clock64() - (t0)))
 #else
 #define PROF_T(v)
 #define PROF_ADD(slot, t0)
 #endif
-
-// Input rows [first, end) of full-row band k (band rows 0 .. IN_ROWS-1 = image rows
-// OUT_ROWS*k - 1 ...) that lie inside the image; the others are the zero padding.
-template <int TW>
-__device__ __forceinline__ int2 band_rows(int k, int H) {
-  const int r0 = Geo<TW>::OUT_ROWS * k - 1;
-  return make_int2(r0 < 0 ? -r0 : 0, min(Geo<TW>::IN_ROWS, H - r0));
-}
 
 struct TcParams {
   const uint8_t* xh;  // packed X tiles [n][band][chunk] (hi), XTILE bytes each
@@ -144,107 +167,149 @@ __device__ __forceinline__ void tmem_ld8(uint32_t taddr, float* v) {
 }
 
 // ---- pooling epilogue ------------------------------------------------------------------
-// max-fold of rotations [R0, R0+G) of this base into Yr[R0] (+ argmax, ties -> smallest
-// index); in place to keep the register footprint at Y + staging.
-template <int R0, int G>
-__device__ __forceinline__ void fold_max(float (&Yr)[4][XH], uint32_t (&arg)[XH / 4], int kk0) {
+// Generic in NX, the pixels of one row segment (16 from registers, 4 for a carried row read
+// back from TMEM in chunks).
+// max-fold of rotations [R0, R0+G) of this base into Yr[R0] (+ argmax a[] per pixel, ties ->
+// smallest index); in place to keep the register footprint at Y + staging.  Branch-free
+// selects: data-dependent branches here cost several times the compares.
+template <int R0, int G, int NX, int RPB>
+__device__ __forceinline__ void fold_max(float (&Yr)[RPB][NX], uint32_t (&a)[NX], int kk0) {
 #pragma unroll
   for (int r = R0 + 1; r < R0 + G; ++r)
 #pragma unroll
-    for (int j = 0; j < XH; ++j)
-      if (Yr[r][j] > Yr[R0][j]) {
-        Yr[R0][j] = Yr[r][j];
-        arg[j / 4] = (arg[j / 4] & ~(0xFFu << (8 * (j % 4)))) | ((uint32_t)(kk0 + r - R0) << (8 * (j % 4)));
-      }
+    for (int j = 0; j < NX; ++j) {
+      const bool gt = Yr[r][j] > Yr[R0][j];
+      Yr[R0][j] = gt ? Yr[r][j] : Yr[R0][j];
+      a[j] = gt ? (uint32_t)(kk0 + r - R0) : a[j];
+    }
 }
-__device__ __forceinline__ void store8(float* dst, const float (&v)[XH]) {
+template <int NX>
+__device__ __forceinline__ void store_vec(float* dst, const float (&v)[NX]) {
   float4* d4 = reinterpret_cast<float4*>(dst);
 #pragma unroll
-  for (int k = 0; k < XH / 4; ++k) d4[k] = make_float4(v[4 * k], v[4 * k + 1], v[4 * k + 2], v[4 * k + 3]);
+  for (int k = 0; k < NX / 4; ++k) d4[k] = make_float4(v[4 * k], v[4 * k + 1], v[4 * k + 2], v[4 * k + 3]);
 }
-__device__ __forceinline__ void store_row(const TcParams& p, size_t off, float (&v)[XH],
-                                          const uint32_t (&arg)[XH / 4], float bz, bool fin) {
+template <int NX>
+__device__ __forceinline__ void store_row(const TcParams& p, size_t off, float (&v)[NX], const uint32_t (&a)[NX],
+                                          float bz, bool fin) {
   if (fin) {
 #pragma unroll
-    for (int j = 0; j < XH; ++j) v[j] += bz;
+    for (int j = 0; j < NX; ++j) v[j] += bz;
     if (p.act == RC_ACT_RELU) {
 #pragma unroll
-      for (int j = 0; j < XH; ++j) v[j] = fmaxf(v[j], 0.f);
+      for (int j = 0; j < NX; ++j) v[j] = fmaxf(v[j], 0.f);
     }
   }
-  store8(p.y + off, v);
-  if (p.am) *reinterpret_cast<uint4*>(p.am + off) = make_uint4(arg[0], arg[1], arg[2], arg[3]);
+  uint32_t arg[NX / 4];  // argmax bytes, little-endian: pixel j in byte j % 4 of word j / 4
+#pragma unroll
+  for (int k = 0; k < NX / 4; ++k) arg[k] = a[4 * k] | (a[4 * k + 1] << 8) | (a[4 * k + 2] << 16) | (a[4 * k + 3] << 24);
+#if RC_TC_ABLATE_FIN == 2  // experiment: pooled, but one float stored per row (wrong results)
+  {
+    float acc = 0.f;
+#pragma unroll
+    for (int j = 0; j < NX; ++j) acc += v[j] + (float)arg[j / 4];
+    p.y[off] = acc;
+    return;
+  }
+#endif
+  store_vec<NX>(p.y + off, v);
+  if (p.am) {
+    if constexpr (NX % 16 == 0) {
+#pragma unroll
+      for (int k = 0; k < NX / 16; ++k)
+        reinterpret_cast<uint4*>(p.am + off)[k] = make_uint4(arg[4 * k], arg[4 * k + 1], arg[4 * k + 2], arg[4 * k + 3]);
+    } else {
+#pragma unroll
+      for (int k = 0; k < NX / 4; ++k) reinterpret_cast<uint32_t*>(p.am + off)[k] = arg[k];
+    }
+  }
 }
 
-// pool + bias + store one output row (16 px) of base b; same semantics as ri_simt.cu.
-// Fold groups gf in {1, 2, 4} stay inside a base; gf % 4 == 0 spans bases through a
-// partial (value, argmax) kept in the output row itself (same thread, program order).
-template <int TW, int RPB>
-__device__ __forceinline__ void finalize_row(const TcParams& p, float (&Yr)[RPB][XH], int n, int co, int b,
-                                             int row, int x0) {
+// pool + bias + store NX output pixels [x0, x0+NX) of one row of base b; same semantics
+// as ri_simt.cu.  Fold groups gf in {1, 2, 4} stay inside a base; gf % 4 == 0 spans bases
+// through a partial (value, argmax) kept in the output row itself (same thread, program
+// order).
+// bz = bias[co] (0 without bias), loaded once per work item by the caller
+#ifndef RC_TC_ABLATE_FIN  // experiment: 1 = no pooling (one float per row stored; wrong results)
+#define RC_TC_ABLATE_FIN 0
+#endif
+template <int TW, int RPB, int NX>
+__device__ __forceinline__ void finalize_row(const TcParams& p, float (&Yr)[RPB][NX], int n, int co, int b,
+                                             int row, int x0, float bz) {
   const int wimg = TW ? TW : p.W;
   const size_t plane = (size_t)p.H * wimg;
   const size_t ybase = ((size_t)n * p.Cout + co) * p.RO * plane + (size_t)row * wimg + x0;
-  const float bz = p.bias ? p.bias[co] : 0.f;
+#if RC_TC_ABLATE_FIN == 1
+  {
+    float acc = bz;
+#pragma unroll
+    for (int r = 0; r < RPB; ++r)
+#pragma unroll
+      for (int j = 0; j < NX; ++j) acc += Yr[r][j];
+    p.y[ybase] = acc;
+    return;
+  }
+#endif
+  uint32_t arg[NX];  // per-pixel argmax (orientation index within the fold group)
+#pragma unroll
+  for (int j = 0; j < NX; ++j) arg[j] = 0;
   if constexpr (RPB == 1) {  // single orientation: every reduction of one slice is the slice
-    const uint32_t z[XH / 4] = {0, 0, 0, 0};
-    store_row(p, ybase, Yr[0], z, bz, true);
+    store_row<NX>(p, ybase, Yr[0], arg, bz, true);
     return;
   } else {
   if (p.pool == RC_POOL_NONE) {
-    const uint32_t z[XH / 4] = {0, 0, 0, 0};
 #pragma unroll
-    for (int r = 0; r < 4; ++r) store_row(p, ybase + (size_t)(b * 4 + r) * plane, Yr[r], z, bz, true);
+    for (int r = 0; r < 4; ++r) store_row<NX>(p, ybase + (size_t)(b * 4 + r) * plane, Yr[r], arg, bz, true);
     return;
   }
   if (p.pool == RC_POOL_AVG) {
     if (b > 0) {
 #pragma unroll
-      for (int j = 0; j < XH; ++j) Yr[0][j] = p.y[ybase + j] + Yr[0][j];
+      for (int j = 0; j < NX; ++j) Yr[0][j] = p.y[ybase + j] + Yr[0][j];
     }
 #pragma unroll
     for (int r = 1; r < 4; ++r)
 #pragma unroll
-      for (int j = 0; j < XH; ++j) Yr[0][j] += Yr[r][j];
+      for (int j = 0; j < NX; ++j) Yr[0][j] += Yr[r][j];
     if (b == p.NB - 1) {  // R is a power of two here (tc_supported): x * (1/R) == x / R exactly
 #pragma unroll
-      for (int j = 0; j < XH; ++j) Yr[0][j] = __fadd_rn(__fmul_rn(Yr[0][j], p.inv_r), bz);
+      for (int j = 0; j < NX; ++j) Yr[0][j] = __fadd_rn(__fmul_rn(Yr[0][j], p.inv_r), bz);
       if (p.act == RC_ACT_RELU) {
 #pragma unroll
-        for (int j = 0; j < XH; ++j) Yr[0][j] = fmaxf(Yr[0][j], 0.f);
+        for (int j = 0; j < NX; ++j) Yr[0][j] = fmaxf(Yr[0][j], 0.f);
       }
     }
-    store8(p.y + ybase, Yr[0]);
+    store_vec<NX>(p.y + ybase, Yr[0]);
     return;
   }
   const int gf = p.gf;
-  uint32_t arg[XH / 4] = {0, 0, 0, 0};
   if (gf == 1) {
 #pragma unroll
-    for (int r = 0; r < 4; ++r) store_row(p, ybase + (size_t)(b * 4 + r) * plane, Yr[r], arg, bz, true);
+    for (int r = 0; r < 4; ++r) store_row<NX>(p, ybase + (size_t)(b * 4 + r) * plane, Yr[r], arg, bz, true);
   } else if (gf == 2) {
-    fold_max<0, 2>(Yr, arg, 0);
-    store_row(p, ybase + (size_t)(b * 2) * plane, Yr[0], arg, bz, true);
-    arg[0] = arg[1] = arg[2] = arg[3] = 0;
-    fold_max<2, 2>(Yr, arg, 0);
-    store_row(p, ybase + (size_t)(b * 2 + 1) * plane, Yr[2], arg, bz, true);
+    fold_max<0, 2, NX>(Yr, arg, 0);
+    store_row<NX>(p, ybase + (size_t)(b * 2) * plane, Yr[0], arg, bz, true);
+#pragma unroll
+    for (int j = 0; j < NX; ++j) arg[j] = 0;
+    fold_max<2, 2, NX>(Yr, arg, 0);
+    store_row<NX>(p, ybase + (size_t)(b * 2 + 1) * plane, Yr[2], arg, bz, true);
   } else {  // gf % 4 == 0
     const int o0 = b * 4, slot = o0 / gf, kk0 = o0 - slot * gf;
     const size_t off = ybase + (size_t)slot * plane;
-    arg[0] = arg[1] = arg[2] = arg[3] = (uint32_t)kk0 * 0x01010101u;  // candidate r=0 is index kk0
-    fold_max<0, 4>(Yr, arg, kk0);
+#pragma unroll
+    for (int j = 0; j < NX; ++j) arg[j] = (uint32_t)kk0;  // candidate r = 0 is index kk0
+    fold_max<0, 4, NX>(Yr, arg, kk0);
     if (kk0 > 0) {  // continue the slot begun in an earlier base
 #pragma unroll
-      for (int j = 0; j < XH; ++j) {
+      for (int j = 0; j < NX; ++j) {
         const float prev = p.y[off + j];
         const uint32_t pa = p.am ? p.am[off + j] : 0u;
-        if (!(Yr[0][j] > prev)) {  // earlier (smaller) index wins ties
-          Yr[0][j] = prev;
-          arg[j / 4] = (arg[j / 4] & ~(0xFFu << (8 * (j % 4)))) | (pa << (8 * (j % 4)));
-        }
+        const bool keep = !(Yr[0][j] > prev);  // earlier (smaller) index wins ties
+        Yr[0][j] = keep ? prev : Yr[0][j];
+        arg[j] = keep ? pa : arg[j];
       }
     }
-    store_row(p, off, Yr[0], arg, bz, kk0 + 4 == gf);
+    store_row<NX>(p, off, Yr[0], arg, bz, kk0 + 4 == gf);
   }
   }
 }
@@ -269,14 +334,6 @@ __device__ __forceinline__ void scatter_row(float (&Y)[RPB][XH], const float (&z
       Y[r][x] += z[src];
     }
   }
-}
-
-__device__ __forceinline__ void tmem_zero32(uint32_t taddr) {  // columns [0, 32) of the warp's lanes
-#pragma unroll
-  for (int c = 0; c < 32; c += 8)
-    asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%1,%1,%1,%1,%1,%1,%1};\n" ::"r"(taddr + c), "r"(0u)
-                 : "memory");
-  asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
 }
 
 // one input row of a strip thread's window: the two halo columns after its 16
@@ -354,9 +411,7 @@ struct EpiState {
   int db;
   uint32_t dph;
   int lane;
-  int o0;              // small images: first output row of the thread (within its image)
-  int vmask;           // window rows 0..2 inside the image (bit I); the others were not computed
-  uint32_t zero_addr;  // TMEM columns [0, D0) of the thread's lane: zeros (full-row bands)
+  int o0;  // small images: first output row of the thread (within its image)
 };
 
 __device__ __forceinline__ void release_d(EpiState& e, int ndb, uint64_t* d_empty) {
@@ -369,7 +424,8 @@ __device__ __forceinline__ void release_d(EpiState& e, int ndb, uint64_t* d_empt
   }
 }
 
-// one tap (compile-time T): three single-row TMEM round trips, D released after the last
+// one tap (compile-time T) of the halo-band geometries (strips, small images): the window
+// rows from TMEM, D released after the last load
 template <int TW, int RPB, int CONV, int T>
 __device__ __forceinline__ void epi_tap(EpiState& e, float (&Y)[RPB][XH], uint64_t* d_full, uint64_t* d_empty) {
   constexpr int NDB = Geo<TW>::NDB;
@@ -389,16 +445,6 @@ __device__ __forceinline__ void epi_tap(EpiState& e, float (&Y)[RPB][XH], uint64
     if constexpr (TR >= 4) small_row<TW, RPB, CONV, T, 5>(a, e.o0, Y);
     release_d(e, NDB, d_empty);
     return;
-  }
-  const int m = e.vmask;  // window rows outside the image were not computed: read zeros
-  if constexpr (TW == 16) {
-    // one window row at a time: a TMEM round trip is ~22 cycles, and a single 16-value row
-    // in flight keeps the epilogue's registers (Y = 64) clear of spills, which would share
-    // the L1/shared-memory bandwidth the SS MMAs are bound by
-    load_row<TW>((m & 1) ? a : e.zero_addr, z);
-    scatter_row<TW, RPB, CONV, T, 0>(Y, z);
-    load_row<TW>((m & 2) ? a + Geo<TW>::RS : e.zero_addr, z);
-    scatter_row<TW, RPB, CONV, T, 1>(Y, z);
   } else {  // strips: rows 0 and 1 in flight together
     float z1[18];
     issue_row<TW>(a, z);
@@ -406,17 +452,221 @@ __device__ __forceinline__ void epi_tap(EpiState& e, float (&Y)[RPB][XH], uint64
     tmem_wait_ld();
     scatter_row<TW, RPB, CONV, T, 0>(Y, z);
     scatter_row<TW, RPB, CONV, T, 1>(Y, z1);
+    load_row<TW>(a + 2 * Geo<TW>::RS, z);
+    release_d(e, NDB, d_empty);
+    scatter_row<TW, RPB, CONV, T, 2>(Y, z);
   }
-  load_row<TW>((m & 4) ? a + 2 * Geo<TW>::RS : e.zero_addr, z);
-  release_d(e, NDB, d_empty);
-  scatter_row<TW, RPB, CONV, T, 2>(Y, z);
 }
 
-// Epilogue warp: lane quadrant q (co = q*32 + lane); sub-tile sub = output row of the band.
-// Work schedule: CTA i walks items i, i + grid, ...; item -> (image n, co tile ct) =
-// (item / NCT, item % NCT).
+// ---- 16-wide carry bands ---------------------------------------------------------------
+// D-row i of a CARRY D buffer (input row 4k + i): 16 columns of Z(Xh) (+ Z(Xl), bf16x3)
+template <bool cat>
+__device__ __forceinline__ void load_row_cat(uint32_t a, float (&z)[18]) {
+  float(&zz)[16] = *reinterpret_cast<float(*)[16]>(&z[1]);
+  tmem_ld16(a, zz);
+  if constexpr (cat) {
+    float t[16];
+    tmem_ld16(a + Geo<16>::MMA_N, t);
+    tmem_wait_ld();
+#pragma unroll
+    for (int j = 0; j < 16; ++j) zz[j] += t[j];
+  } else {
+    tmem_wait_ld();
+  }
+}
+
+// scatter one input row into a row state kept in TMEM (carry + r*16 = rotation r, 16 px):
+// read-modify-write of each rotation that takes this row (I = 1 + di, as scatter_row)
+template <int RPB, int CONV, int T, int I>
+__device__ __forceinline__ void rmw_row(uint32_t carry, const float (&z)[18]) {
+  bool wrote = false;
+#pragma unroll
+  for (int r = 0; r < RPB; ++r) {
+    const int di = make_k3(CONV).di[r][T];
+    const int dj = make_k3(CONV).dj[r][T];
+    if (1 + di != I) continue;
+    float c[16];
+    tmem_ld16(carry + r * 16, c);
+    tmem_wait_ld();
+#pragma unroll
+    for (int x = 0; x < 16; ++x) {
+      const int src = x + dj + 1;
+      if (src < 1 || src > 16) continue;
+      c[x] += z[src];
+    }
+    tmem_st16(carry + r * 16, c);
+    wrote = true;
+  }
+  if (wrote) tmem_wait_st();
+}
+
+// One tap of a 16-wide carry band k.  The 2 warps of a lane quadrant (half h) each own two
+// output rows in registers (Y0, Y1) and one carried row in TMEM:
+//   h = 0: Y0 = row 4k   (D-rows 0, 1; its input row 4k-1 came in as carry B),
+//          Y1 = row 4k+1 (D-rows 0, 1, 2), TMEM carry B = row 4k+4 (D-row 3)
+//   h = 1: Y0 = row 4k+2 (D-rows 1, 2, 3), Y1 = row 4k+3 (D-rows 2, 3),
+//          TMEM carry A = row 4k-1 (D-row 0; k > 0)
+// Each thread reads the 4 D-rows once per tap.  I = 1 + di selects the rotations of tap T
+// that read the row (scatter_row).
+template <int RPB, int CONV, int H, int T, bool cat>
+__device__ __forceinline__ void epi_tap_carry(EpiState& e, float (&Y0)[RPB][XH], float (&Y1)[RPB][XH],
+                                              bool first_band, uint32_t carry, uint64_t* d_full,
+                                              uint64_t* d_empty) {
+  using G = Geo<16>;
+  const uint32_t a = e.row_base + e.db * G::DCOLS;
+  float z[18];
+  PROF_T(t_df);
+  mbar_wait(&d_full[e.db], e.dph);
+  if (threadIdx.x / 32 == EPI_WARP0) PROF_ADD(11, t_df);
+  if (threadIdx.x / 32 == EPI_WARP0 + 4) PROF_ADD(17, t_df);
+  tc_fence_after();
+  if constexpr (H == 0) {
+    load_row_cat<cat>(a, z);
+    scatter_row<16, RPB, CONV, T, 1>(Y0, z);
+    scatter_row<16, RPB, CONV, T, 0>(Y1, z);
+    load_row_cat<cat>(a + 16, z);
+    scatter_row<16, RPB, CONV, T, 2>(Y0, z);
+    scatter_row<16, RPB, CONV, T, 1>(Y1, z);
+    load_row_cat<cat>(a + 32, z);
+    scatter_row<16, RPB, CONV, T, 2>(Y1, z);
+    load_row_cat<cat>(a + 48, z);
+    release_d(e, G::NDB, d_empty);
+    rmw_row<RPB, CONV, T, 0>(carry, z);
+  } else {
+    load_row_cat<cat>(a + 16, z);
+    scatter_row<16, RPB, CONV, T, 0>(Y0, z);
+    load_row_cat<cat>(a + 32, z);
+    scatter_row<16, RPB, CONV, T, 1>(Y0, z);
+    scatter_row<16, RPB, CONV, T, 0>(Y1, z);
+    load_row_cat<cat>(a + 48, z);
+    scatter_row<16, RPB, CONV, T, 2>(Y0, z);
+    scatter_row<16, RPB, CONV, T, 1>(Y1, z);
+    if (first_band) {
+      release_d(e, G::NDB, d_empty);
+    } else {
+      load_row_cat<cat>(a, z);
+      release_d(e, G::NDB, d_empty);
+      rmw_row<RPB, CONV, T, 2>(carry, z);
+    }
+  }
+}
+
+// h = 1 at the end of band k > 0: output row 4k-1 lives in TMEM carry A; pool + store it
+// in chunks of 4 pixels
+// (the TMEM loads are warp-collective, .sync.aligned: every lane loads, only live lanes,
+// co < Cout, store)
+template <int RPB>
+__device__ __forceinline__ void finalize_carried(const TcParams& p, uint32_t carry, int n, int co, int b, int row,
+                                                 bool live, float bz) {
+#pragma unroll 1
+  for (int c4 = 0; c4 < 4; ++c4) {
+    float Yc[RPB][4];
+#pragma unroll
+    for (int r = 0; r < RPB; ++r) tmem_ld4(carry + r * 16 + c4 * 4, Yc[r]);
+    tmem_wait_ld();
+    if (live) finalize_row<16, RPB, 4>(p, Yc, n, co, b, row, c4 * 4, bz);
+  }
+}
+
+template <int RPB, int CONV, int H, bool P3>
+__device__ __forceinline__ void epilogue_carry_half(const TcParams& p, uint32_t tmem, uint64_t* d_full,
+                                                    uint64_t* d_empty) {
+  using G = Geo<16>;
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int q = warp % 4;
+  const int co_l = q * 32 + lane;
+  const uint32_t lanes = tmem + ((uint32_t)(q * 32) << 16);
+  const uint32_t carry = lanes + (H == 1 ? 0u : 64u);  // TMEM columns [0, 64): carry A, [64, 128): carry B
+  constexpr bool cat = G::CAT && P3;
+  EpiState e{lanes + G::D0, 0, 0, lane, 0};
+  float Y0[RPB][XH], Y1[RPB][XH];
+  PROF_T(t_epi0);
+  for (int item = blockIdx.x; item < p.items; item += gridDim.x) {
+    const int n = item / p.NCT, ct = item % p.NCT;
+    const int co = ct * 128 + co_l;
+    const bool live = co < p.Cout;
+    const float bz = (live && p.bias) ? p.bias[co] : 0.f;
+    for (int b = 0; b < p.NB; ++b)
+      for (int k = 0; k < p.NBK; ++k) {
+        const bool first = k == 0, last = k == p.NBK - 1;
+        if (H == 0 && !first) {  // row 4k: its input row 4k-1 was scattered in band k-1
+#pragma unroll
+          for (int r = 0; r < RPB; ++r) tmem_ld16(carry + r * 16, Y0[r]);
+          tmem_wait_ld();
+        } else {
+#pragma unroll
+          for (int r = 0; r < RPB; ++r)
+#pragma unroll
+            for (int x = 0; x < XH; ++x) Y0[r][x] = 0.f;
+        }
+#pragma unroll
+        for (int r = 0; r < RPB; ++r)
+#pragma unroll
+          for (int x = 0; x < XH; ++x) Y1[r][x] = 0.f;
+        if (H == 0) {  // carry B restarts for row 4k+4
+#pragma unroll
+          for (int r = 0; r < RPB; ++r) tmem_st16_zero(carry + r * 16);
+          tmem_wait_st();
+        }
+        epi_tap_carry<RPB, CONV, H, 0, cat>(e, Y0, Y1, first, carry, d_full, d_empty);
+        epi_tap_carry<RPB, CONV, H, 1, cat>(e, Y0, Y1, first, carry, d_full, d_empty);
+        epi_tap_carry<RPB, CONV, H, 2, cat>(e, Y0, Y1, first, carry, d_full, d_empty);
+        epi_tap_carry<RPB, CONV, H, 3, cat>(e, Y0, Y1, first, carry, d_full, d_empty);
+        epi_tap_carry<RPB, CONV, H, 4, cat>(e, Y0, Y1, first, carry, d_full, d_empty);
+        epi_tap_carry<RPB, CONV, H, 5, cat>(e, Y0, Y1, first, carry, d_full, d_empty);
+        epi_tap_carry<RPB, CONV, H, 6, cat>(e, Y0, Y1, first, carry, d_full, d_empty);
+        epi_tap_carry<RPB, CONV, H, 7, cat>(e, Y0, Y1, first, carry, d_full, d_empty);
+        epi_tap_carry<RPB, CONV, H, 8, cat>(e, Y0, Y1, first, carry, d_full, d_empty);
+        PROF_T(t_fin);
+        // Rows to store: h = 0 rows 4k, 4k+1; h = 1 the carried row 4k-1 (k > 0), row 4k+2 and,
+        // in the last band (input row 4k+4 is padding), row 4k+3 -- otherwise row 4k+3
+        // continues in band k+1 through carry A.  One finalize call site per half (a rolled
+        // loop moving Y1 into Y0): the pooling code is large and runs once per band, so
+        // inlined copies would only evict the tap loop from the instruction cache.
+        int nrows = 2;
+        if constexpr (H == 1) {
+          if (!first && 4 * k - 1 < p.H) finalize_carried<RPB>(p, carry, n, co, b, 4 * k - 1, live, bz);
+          if (!last) {
+#pragma unroll
+            for (int r = 0; r < RPB; ++r) tmem_st16(carry + r * 16, Y1[r]);
+            tmem_wait_st();
+            nrows = 1;
+          }
+        }
+#pragma unroll 1
+        for (int i = 0; i < nrows; ++i) {
+          const int row = 4 * k + 2 * H + i;
+          if (live && row < p.H) finalize_row<16, RPB, XH>(p, Y0, n, co, b, row, 0, bz);
+          if (i == 0) {
+#pragma unroll
+            for (int r = 0; r < RPB; ++r)
+#pragma unroll
+              for (int x = 0; x < XH; ++x) Y0[r][x] = Y1[r][x];
+          }
+        }
+        if (warp == EPI_WARP0) PROF_ADD(12, t_fin);
+        if (warp == EPI_WARP0 + 4) PROF_ADD(18, t_fin);
+      }
+  }
+  if (warp == EPI_WARP0) PROF_ADD(10, t_epi0);
+  if (warp == EPI_WARP0 + 4) PROF_ADD(16, t_epi0);
+}
+
+// the 8 epilogue warps of a carry kernel: half h = (warp - 4) / 4 of its lane quadrant
+// (compile time below the dispatch: each half's band loop is straight-line code)
+template <int RPB, int CONV, bool P3>
+__device__ __forceinline__ void epilogue_carry(const TcParams& p, uint32_t tmem, uint64_t* d_full, uint64_t* d_empty) {
+  if ((threadIdx.x / 32 - EPI_WARP0) / 4 == 0)
+    epilogue_carry_half<RPB, CONV, 0, P3>(p, tmem, d_full, d_empty);
+  else
+    epilogue_carry_half<RPB, CONV, 1, P3>(p, tmem, d_full, d_empty);
+}
+
+// Epilogue warp of the halo-band geometries: lane quadrant q (co = q*32 + lane); sub-tile
+// sub = output row of the band.  Work schedule: CTA i walks items i, i + grid, ...; item ->
+// (image n, co tile ct) = (item / NCT, item % NCT).
 template <int TW, int RPB, int CONV>
-__device__ void epilogue(const TcParams& p, uint32_t tmem, uint64_t* d_full, uint64_t* d_empty) {
+__device__ __forceinline__ void epilogue(const TcParams& p, uint32_t tmem, uint64_t* d_full, uint64_t* d_empty) {
   using G = Geo<TW>;
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int q = warp % 4;
@@ -427,28 +677,20 @@ __device__ void epilogue(const TcParams& p, uint32_t tmem, uint64_t* d_full, uin
   const int s_img = G::SMALL ? (G::IMGS > 1 ? sub : 0) : 0;
   const int o0 = G::SMALL ? (G::IMGS > 1 ? 0 : sub * G::TR) : 0;
   const uint32_t rb = G::SMALL ? (uint32_t)((s_img * TW + o0) * G::RS) : (uint32_t)(srow * G::RS);
-  EpiState e{tmem + ((uint32_t)(q * 32) << 16) + G::D0 + rb, 0, 0, lane, o0, 7,
-             tmem + ((uint32_t)(q * 32) << 16) + 1};
-  if constexpr (G::TRIM) tmem_zero32(tmem + ((uint32_t)(q * 32) << 16));  // every warp of the quadrant
-                                                                           // writes the same zeros
+  EpiState e{tmem + ((uint32_t)(q * 32) << 16) + G::D0 + rb, 0, 0, lane, o0};
   const int nstrip = G::STRIP ? p.W / 16 : 1;
   float Y[RPB][XH];
   PROF_T(t_epi0);
   for (int item = blockIdx.x; item < p.items; item += gridDim.x) {
     const int n = item / p.NCT, ct = item % p.NCT;
     const int co = ct * 128 + co_l;
+    const float bz = (co < p.Cout && p.bias) ? p.bias[co] : 0.f;
     for (int k = 0; k < p.NBK; ++k)
       for (int b = 0; b < p.NB; ++b) {
 #pragma unroll
         for (int r = 0; r < RPB; ++r)
 #pragma unroll
           for (int x = 0; x < XH; ++x) Y[r][x] = 0.f;
-        if constexpr (G::TRIM) {
-          const int2 v = band_rows<TW>(k, p.H);
-          e.vmask = 0;
-#pragma unroll
-          for (int i = 0; i < 3; ++i) e.vmask |= (srow + i >= v.x && srow + i < v.y) ? 1 << i : 0;
-        }
         epi_tap<TW, RPB, CONV, 0>(e, Y, d_full, d_empty);
         epi_tap<TW, RPB, CONV, 1>(e, Y, d_full, d_empty);
         epi_tap<TW, RPB, CONV, 2>(e, Y, d_full, d_empty);
@@ -462,7 +704,7 @@ __device__ void epilogue(const TcParams& p, uint32_t tmem, uint64_t* d_full, uin
         const int x0 = G::SMALL ? 0 : (k % nstrip) * 16;
         const int img = G::SMALL ? n * G::IMGS + s_img : n;  // small: n indexes bands of IMGS images
         PROF_T(t_fin);
-        if (img < p.N && co < p.Cout && row < p.H) finalize_row<TW, RPB>(p, Y, img, co, b, row, x0);
+        if (img < p.N && co < p.Cout && row < p.H) finalize_row<TW, RPB, XH>(p, Y, img, co, b, row, x0, bz);
         if (warp == EPI_WARP0) PROF_ADD(12, t_fin);
       }
   }
@@ -482,8 +724,9 @@ struct Ring {
   }
 };
 
-template <int TW, int RPB, int CONV>
-__global__ void __launch_bounds__(THREADS, 1) ri_tc_kernel(const __grid_constant__ TcParams p) {
+// P3: bf16x3 (three products) -- compile time for the CARRY epilogue's [Xh | Xl] row sums
+template <int TW, int RPB, int CONV, bool P3>
+__global__ void __launch_bounds__(Epi<TW>::THREADS, 1) ri_tc_kernel(const __grid_constant__ TcParams p) {
   using G = Geo<TW>;
   constexpr int NDB = G::NDB;
   constexpr int XS = G::XTILE;                        // bytes of a band tile
@@ -512,7 +755,7 @@ __global__ void __launch_bounds__(THREADS, 1) ri_tc_kernel(const __grid_constant
     }
     for (int i = 0; i < NDB; ++i) {
       mbar_init(&d_full[i], 1);
-      mbar_init(&d_empty[i], NUM_EPI);
+      mbar_init(&d_empty[i], Epi<TW>::WARPS);
     }
     fence_barrier_init();
   }
@@ -529,7 +772,26 @@ __global__ void __launch_bounds__(THREADS, 1) ri_tc_kernel(const __grid_constant
   const int stage_bytes = stage_w + (p.xstream ? p.spc * parts * XS : 0);
   const int stages_per_tap = p.NC / p.spc;
   const int S0 = (S + 1) / 2;  // ring 0 (MMA warp 1): slots [0, S0); ring 1 (MMA warp 2): [S0, S)
-  if (warp < EPI_WARP0) asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(REGS_PRODUCER));
+  // X chunk c of a region of `cnt` chunks (the resident band: NC; a streamed stage: spc).
+  // CARRY: [Xh rows | Xl rows] of a chunk are adjacent (one N = 128 B operand, one copy);
+  // otherwise [hi chunks][lo chunks].
+  // (lambdas capture scalars by value: a by-reference capture of the __grid_constant__ params
+  // would turn every later p.field read into a generic memory load)
+  auto xh_off = [=](int c, int cnt) -> uint32_t { return (uint32_t)(G::CARRY ? c * parts * XS : c * XS); };
+  auto xl_off = [=](int c, int cnt) -> uint32_t {
+    return (uint32_t)(G::CARRY ? c * parts * XS + XS : (cnt + c) * XS);
+  };
+  // Band schedule of a work item: units u = (band k, base b).  CARRY bands walk the bases
+  // outermost (the carried rows belong to one base) and reload X per unit; halo bands keep X
+  // resident across the bases of a band.
+  const int NB = p.NB, NBK = p.NBK;
+  const int units = NB * NBK;
+  auto unit_k = [=](int u) { return G::CARRY ? u % NBK : u / NB; };
+  auto unit_b = [=](int u) { return G::CARRY ? u / NBK : u % NB; };
+  auto x_first = [=](int u) { return G::CARRY || unit_b(u) == 0; };      // unit loads a new X band
+  auto x_last = [=](int u) { return G::CARRY || unit_b(u) == NB - 1; };  // last unit on this X band
+  const int taps_per_band = G::CARRY ? 9 : p.NB * 9;                          // taps per X band
+  if (warp < EPI_WARP0) asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(Epi<TW>::PROD));
   if (warp == 0 || warp == 3) {
     // ------------------------------------------------------------ producers (whole warp
     // walks the schedule in MMA consumption order; one elected lane issues the copies).
@@ -540,49 +802,69 @@ __global__ void __launch_bounds__(THREADS, 1) ri_tc_kernel(const __grid_constant
     uint32_t xc = 0, gd = 0;  // bands loaded so far (phase of the per-chunk X barriers), global tap
     for (int item = blockIdx.x; item < p.items; item += gridDim.x) {
       const int n = item / p.NCT, ct = item % p.NCT;
-      for (int k = 0; k < p.NBK; ++k) {
+      for (int u = 0; u < units; ++u) {
+        const int k = unit_k(u), b = unit_b(u);
         const size_t tile = ((size_t)n * p.NBK + k) * p.NC;
-        if (me == 0 && !p.xstream) {  // new band: its X chunks (both MMA warps read them)
+        if (me == 0 && !p.xstream && x_first(u)) {  // new band: its X chunks (both MMA warps read them)
           for (int c = 0; c < p.NC; ++c) {
             PROF_T(t_xe);
             if (xc > 0) mbar_wait(&x_empty[c], (xc - 1) & 1);
             PROF_ADD(14, t_xe);
             if (elect_one()) {
+#if RC_TC_ABLATE_X  // experiment: X loaded once per CTA (stale bands later; wrong results)
+              if (xc > 0) {
+                mbar_arrive(&x_full[c]);
+              } else
+#endif
+              {
               mbar_arrive_expect_tx(&x_full[c], parts * XS);
-              bulk_g2s(xs + c * XS, p.xh + (tile + c) * XS, XS, &x_full[c]);
-              if (parts == 2) bulk_g2s(xs + (p.NC + c) * XS, p.xl + (tile + c) * XS, XS, &x_full[c]);
+              if (G::CARRY) {
+                bulk_g2s(xs + xh_off(c, p.NC), p.xh + (tile + c) * parts * XS, parts * XS, &x_full[c]);
+              } else {
+                bulk_g2s(xs + xh_off(c, p.NC), p.xh + (tile + c) * XS, XS, &x_full[c]);
+                if (parts == 2) bulk_g2s(xs + xl_off(c, p.NC), p.xl + (tile + c) * XS, XS, &x_full[c]);
+              }
+              }
             }
             __syncwarp();
           }
         }
-        for (int b = 0; b < p.NB; ++b) {
-          const uint8_t* wsrc = p.w + (((size_t)b * p.NCT + ct) * 9) * p.NC * parts * WTILE;
-          for (int t = 0; t < 9; ++t, ++gd) {
-            if ((gd & 1u) != me) continue;
-            for (int sp = 0; sp < stages_per_tap; ++sp) {
-              const int st = t * stages_per_tap + sp;
-              PROF_T(t_we);
-              if (wr.used) mbar_wait(&w_empty[base + wr.s], wr.ph ^ 1);
-              PROF_ADD(me == 0 ? 13 : 15, t_we);
-              if (elect_one()) {
-                uint64_t* full = &w_full[base + wr.s];
-                mbar_arrive_expect_tx(full, stage_bytes);
-                uint8_t* dst = ws + (base + wr.s) * stage_bytes;
-                bulk_g2s(dst, wsrc + (size_t)st * stage_w, stage_w, full);
-                if (p.xstream) {  // the stage's X chunks travel with it (re-read from L2 per tap)
-                  const int c0 = sp * p.spc;
-                  for (int cl = 0; cl < p.spc; ++cl) {
-                    bulk_g2s(dst + stage_w + cl * XS, p.xh + (tile + c0 + cl) * XS, XS, full);
-                    if (parts == 2) bulk_g2s(dst + stage_w + (p.spc + cl) * XS, p.xl + (tile + c0 + cl) * XS, XS, full);
+        const uint8_t* wsrc = p.w + (((size_t)b * p.NCT + ct) * 9) * p.NC * parts * WTILE;
+        for (int t = 0; t < 9; ++t, ++gd) {
+          if ((gd & 1u) != me) continue;
+          for (int sp = 0; sp < stages_per_tap; ++sp) {
+            const int st = t * stages_per_tap + sp;
+            PROF_T(t_we);
+            if (wr.used) mbar_wait(&w_empty[base + wr.s], wr.ph ^ 1);
+            PROF_ADD(me == 0 ? 13 : 15, t_we);
+            if (elect_one()) {
+              uint64_t* full = &w_full[base + wr.s];
+              uint8_t* dst = ws + (base + wr.s) * stage_bytes;
+#if RC_TC_ABLATE_W  // experiment: no weight traffic (stale stage contents; wrong results)
+              mbar_arrive(full);
+#else
+              mbar_arrive_expect_tx(full, stage_bytes);
+              bulk_g2s(dst, wsrc + (size_t)st * stage_w, stage_w, full);
+#endif
+              if (p.xstream) {  // the stage's X chunks travel with it (re-read from L2 per tap)
+                const int c0 = sp * p.spc;
+                for (int cl = 0; cl < p.spc; ++cl) {
+                  if (G::CARRY) {
+                    bulk_g2s(dst + stage_w + xh_off(cl, p.spc), p.xh + (tile + c0 + cl) * parts * XS, parts * XS,
+                             full);
+                  } else {
+                    bulk_g2s(dst + stage_w + xh_off(cl, p.spc), p.xh + (tile + c0 + cl) * XS, XS, full);
+                    if (parts == 2)
+                      bulk_g2s(dst + stage_w + xl_off(cl, p.spc), p.xl + (tile + c0 + cl) * XS, XS, full);
                   }
                 }
               }
-              __syncwarp();
-              wr.adv(S_me);
             }
+            __syncwarp();
+            wr.adv(S_me);
           }
         }
-        ++xc;
+        if (x_last(u)) ++xc;
       }
     }
   } else if (warp == 1 || warp == 2) {
@@ -593,95 +875,89 @@ __global__ void __launch_bounds__(THREADS, 1) ri_tc_kernel(const __grid_constant
     // commits its own MMAs (tcgen05.commit tracks the issuing thread's operations).
     const uint32_t me = (uint32_t)(warp - 1);
     const int S_me = me == 0 ? S0 : S - S0, base = me == 0 ? 0 : S0;
-    const uint32_t idesc = idesc_bf16_f32(128, G::MMA_N);
+    // CAT bf16x3: Wh x [Xh | Xl] (N = 2 * MMA_N) then Wl x Xh (N = MMA_N) into its first half
+    const uint32_t idesc = idesc_bf16_f32(128, (G::CAT && parts == 2) ? 2 * G::MMA_N : G::MMA_N);
+    const uint32_t idesc_n = idesc_bf16_f32(128, G::MMA_N);
     const uint32_t xaddr = smem_u32(xs);
-    const int taps_per_band = p.NB * 9;
     Ring wr;
     uint32_t xc = 0, gd = 0;  // gd: global tap index
     int db = 0;
     uint32_t dph = 0;
     PROF_T(t_mma0);
     for (int item = blockIdx.x; item < p.items; item += gridDim.x) {
-      for (int k = 0; k < p.NBK; ++k) {
-        // full-row bands at the image top / bottom: the halo rows outside the image are zero
-        // padding, so the MMA skips them (N shrinks by RS per row; the epilogue never reads
-        // them, see band_rows)
-        uint32_t idesc_k = idesc, xoff_k = 0, doff_k = 0;
-        if constexpr (G::TRIM) {
-          const int2 v = band_rows<TW>(k, p.H);
-          idesc_k = idesc_bf16_f32(128, (uint32_t)((v.y - v.x) * G::RS));
-          xoff_k = (uint32_t)(v.x * G::RS * 128);
-          doff_k = (uint32_t)(v.x * G::RS);
-        }
-        for (int b = 0; b < p.NB; ++b) {
-          for (int t = 0; t < 9; ++t) {
-            const int tb = b * 9 + t;                       // tap index within the band
-            const bool mine = (gd & 1u) == me;
-            const bool first_mine = tb < 2;                 // this warp's first tap of the band
-            const bool last_mine = tb + 2 >= taps_per_band;  // ... and its last one
-            if (mine) {
-              PROF_T(t_d);
-              if (gd >= (uint32_t)NDB) mbar_wait(&d_empty[db], dph ^ 1);
-              PROF_ADD(5 * me + 1, t_d);
+      for (int u = 0; u < units; ++u) {
+        const int b = unit_b(u);
+        for (int t = 0; t < 9; ++t) {
+          const int tb = (G::CARRY ? 0 : b * 9) + t;      // tap index within the X band
+          const bool mine = (gd & 1u) == me;
+          const bool first_mine = tb < 2;                 // this warp's first tap of the X band
+          const bool last_mine = tb + 2 >= taps_per_band;  // ... and its last one
+          if (mine) {
+            PROF_T(t_d);
+            if (gd >= (uint32_t)NDB) mbar_wait(&d_empty[db], dph ^ 1);
+            PROF_ADD(5 * me + 1, t_d);
+            tc_fence_after();
+            const uint32_t d = tmem + G::D0 + db * G::DCOLS;
+            for (int sp = 0; sp < stages_per_tap; ++sp) {
+              PROF_T(t_x);
+              if (first_mine && !p.xstream)
+                for (int cl = 0; cl < p.spc; ++cl) mbar_wait(&x_full[sp * p.spc + cl], xc & 1);
+              PROF_ADD(5 * me + 2, t_x);
+              PROF_T(t_w);
+              mbar_wait(&w_full[base + wr.s], wr.ph);
+              PROF_ADD(5 * me + 3, t_w);
               tc_fence_after();
-              const uint32_t d = tmem + G::D0 + db * G::DCOLS + doff_k;
-              for (int sp = 0; sp < stages_per_tap; ++sp) {
-                PROF_T(t_x);
-                if (first_mine && !p.xstream)
-                  for (int cl = 0; cl < p.spc; ++cl) mbar_wait(&x_full[sp * p.spc + cl], xc & 1);
-                PROF_ADD(5 * me + 2, t_x);
-                PROF_T(t_w);
-                mbar_wait(&w_full[base + wr.s], wr.ph);
-                PROF_ADD(5 * me + 3, t_w);
-                tc_fence_after();
-                PROF_T(t_i);
-                if (elect_one()) {
-                  const uint32_t wbase = smem_u32(ws + (base + wr.s) * stage_bytes);
-                  // descriptors are linear in the smem address (14-bit field, smem < 256 KB): one
-                  // base per stage, constant strides per chunk
-                  const uint32_t xbase = p.xstream ? wbase + stage_w : xaddr + sp * p.spc * XS;
-                  const uint32_t lo_off = p.xstream ? p.spc * XS : p.NC * XS;
-                  const uint64_t b0 = desc_k_sw128(xbase + xoff_k), a0 = desc_k_sw128(wbase);
-                  for (int cl = 0; cl < p.spc; ++cl) {
-                    const int c = sp * p.spc + cl;
-                    const uint32_t xh_a = xbase + cl * XS, xl_a = xh_a + lo_off;
-                    const uint64_t bh = b0 + (uint32_t)((cl * XS) >> 4);
-                    const uint64_t ah = a0 + (uint32_t)((cl * parts * WTILE) >> 4);
+              PROF_T(t_i);
+              if (elect_one()) {
+                const uint32_t wbase = smem_u32(ws + (base + wr.s) * stage_bytes);
+                // descriptors are linear in the smem address (14-bit field, smem < 256 KB): one
+                // base per stage, constant strides per chunk
+                const uint32_t xbase = p.xstream ? wbase + stage_w : xaddr;
+                const int cbase = p.xstream ? 0 : sp * p.spc, cnt = p.xstream ? p.spc : p.NC;
+                const uint64_t a0 = desc_k_sw128(wbase);
+                for (int cl = 0; cl < p.spc; ++cl) {
+                  const int c = sp * p.spc + cl;
+                  const uint64_t bh = desc_k_sw128(xbase + xh_off(cbase + cl, cnt));
+                  const uint64_t ah = a0 + (uint32_t)((cl * parts * WTILE) >> 4);
 #pragma unroll
-                    for (int kk = 0; kk < 4; ++kk) mma_bf16_ss(d, ah + 2 * kk, bh + 2 * kk, idesc_k, (c | kk) != 0);
-                    if (parts == 2) {
-                      const uint64_t bl = desc_k_sw128(xl_a + xoff_k);
-                      const uint64_t al = desc_k_sw128(wbase + (cl * parts + 1) * WTILE);
+                  for (int kk = 0; kk < 4; ++kk) mma_bf16_ss(d, ah + 2 * kk, bh + 2 * kk, idesc, (c | kk) != 0);
+                  if (parts == 2) {
+                    const uint64_t al = desc_k_sw128(wbase + (cl * parts + 1) * WTILE);
+                    if (!G::CAT) {
+                      const uint64_t bl = desc_k_sw128(xbase + xl_off(cbase + cl, cnt));
 #pragma unroll
-                      for (int kk = 0; kk < 4; ++kk) mma_bf16_ss(d, ah + 2 * kk, bl + 2 * kk, idesc_k, 1);
-#pragma unroll
-                      for (int kk = 0; kk < 4; ++kk) mma_bf16_ss(d, al + 2 * kk, bh + 2 * kk, idesc_k, 1);
+                      for (int kk = 0; kk < 4; ++kk) mma_bf16_ss(d, ah + 2 * kk, bl + 2 * kk, idesc_n, 1);
                     }
-                    if (last_mine && !p.xstream) mma_commit(&x_empty[c]);  // chunk c done by this warp
+#pragma unroll
+                    for (int kk = 0; kk < 4; ++kk) mma_bf16_ss(d, al + 2 * kk, bh + 2 * kk, idesc_n, 1);
                   }
-                  mma_commit(&w_empty[base + wr.s]);
-                  if (sp == stages_per_tap - 1) mma_commit(&d_full[db]);
+                  if (last_mine && !p.xstream) mma_commit(&x_empty[c]);  // chunk c done by this warp
                 }
-                __syncwarp();
-                PROF_ADD(5 * me + 4, t_i);
-                wr.adv(S_me);
+                mma_commit(&w_empty[base + wr.s]);
+                if (sp == stages_per_tap - 1) mma_commit(&d_full[db]);
               }
-            }
-            ++gd;
-            if (++db == NDB) {
-              db = 0;
-              dph ^= 1;
+              __syncwarp();
+              PROF_ADD(5 * me + 4, t_i);
+              wr.adv(S_me);
             }
           }
-          if (b == p.NB - 1) ++xc;
+          ++gd;
+          if (++db == NDB) {
+            db = 0;
+            dph ^= 1;
+          }
         }
+        if (x_last(u)) ++xc;
       }
     }
     PROF_ADD(5 * me, t_mma0);
   } else if (warp >= EPI_WARP0) {
     // ------------------------------------------------------------ epilogue
-    asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(REGS_EPILOGUE));
-    epilogue<TW, RPB, CONV>(p, tmem, d_full, d_empty);
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(Epi<TW>::REGS));
+    if constexpr (G::CARRY)
+      epilogue_carry<RPB, CONV, P3>(p, tmem, d_full, d_empty);
+    else
+      epilogue<TW, RPB, CONV>(p, tmem, d_full, d_empty);
   }
   tc_fence_before();
   __syncthreads();
@@ -696,9 +972,9 @@ __device__ __forceinline__ void split_bf16(float v, __nv_bfloat16& hi, __nv_bflo
 }
 
 // X fp32 NCHW -> SW128 bf16 tiles [n][band][chunk][MMA_N px][64 ci] (hi, lo planes).  Band
-// pixel px is (r = px / RS, cc = px % RS) -> image row k*OUT_ROWS - 1 + r and column
-// cc (full rows) or j*16 - 1 + cc (strip j); pixels outside the image (the padding) and the
-// MMA_N - BAND_PX filler pixels are zero.
+// pixel px is (r = px / RS, cc = px % RS) -> image row k*OUT_ROWS - 1 + r (k*OUT_ROWS + r
+// for CARRY bands) and column cc (full rows) or j*16 - 1 + cc (strip j); pixels outside the
+// image (the padding) and the MMA_N - BAND_PX filler pixels are zero.
 template <int TW>
 __global__ void x_pack_kernel(const float* __restrict__ x, uint8_t* __restrict__ xh,
                               uint8_t* __restrict__ xl, int Cin, int H, int W, int NBK, int NC, int Nimg) {
@@ -715,6 +991,9 @@ __global__ void x_pack_kernel(const float* __restrict__ x, uint8_t* __restrict__
       img = n * G::IMGS + px / (TW * TW);
       row = (px / TW) % TW;
       col = px % TW;
+    } else if constexpr (G::CARRY) {  // input rows [4k, 4k+4), no halo
+      row = k * G::OUT_ROWS + px / G::RS;
+      col = px % G::RS;
     } else {
       row = k * G::OUT_ROWS - 1 + px / G::RS;
       col = G::STRIP ? j * 16 - 1 + px % G::RS : px % G::RS;
@@ -724,8 +1003,10 @@ __global__ void x_pack_kernel(const float* __restrict__ x, uint8_t* __restrict__
   }
   __syncthreads();
   const size_t tidx = ((size_t)n * NBK + bk) * NC + c;
-  uint8_t* oh = xh + tidx * G::XTILE;
-  uint8_t* ol = xl ? xl + tidx * G::XTILE : nullptr;
+  // CARRY: one tile per chunk of [MMA_N hi rows | MMA_N lo rows] (the N = 128 B operand of
+  // Wh x [Xh | Xl]); xl selects the two-part layout.  Otherwise separate hi / lo planes.
+  uint8_t* oh = G::CARRY ? xh + tidx * (xl ? 2 : 1) * G::XTILE : xh + tidx * G::XTILE;
+  uint8_t* ol = !xl ? nullptr : (G::CARRY ? oh + G::XTILE : xl + tidx * G::XTILE);
   for (int i = threadIdx.x; i < G::MMA_N * (KC / 8); i += blockDim.x) {
     const int px = i / (KC / 8), g = i % (KC / 8);
     __align__(16) __nv_bfloat16 h8[8], l8[8];
@@ -947,19 +1228,30 @@ int launch_tc(const rc_desc& d, const float* x, const void* bank, const float* b
   int dev, sms;
   RC_CUDA(cudaGetDevice(&dev));
   RC_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-  // [geometry][single][convention]
-  static void (*const kernels[5][2][2])(TcParams) = {
-      {{ri_tc_kernel<16, 4, 0>, ri_tc_kernel<16, 4, 1>}, {ri_tc_kernel<16, 1, 0>, ri_tc_kernel<16, 1, 1>}},
-      {{nullptr, nullptr}, {nullptr, nullptr}},
-      {{ri_tc_kernel<0, 4, 0>, ri_tc_kernel<0, 4, 1>}, {ri_tc_kernel<0, 1, 0>, ri_tc_kernel<0, 1, 1>}},
-      {{ri_tc_kernel<8, 4, 0>, ri_tc_kernel<8, 4, 1>}, {ri_tc_kernel<8, 1, 0>, ri_tc_kernel<8, 1, 1>}},
-      {{ri_tc_kernel<4, 4, 0>, ri_tc_kernel<4, 4, 1>}, {ri_tc_kernel<4, 1, 0>, ri_tc_kernel<4, 1, 1>}}};
+  // [geometry][single][convention][bf16x3]
+#define RC_TC_K(TW, RPB, CONV) {ri_tc_kernel<TW, RPB, CONV, false>, ri_tc_kernel<TW, RPB, CONV, true>}
+  static void (*const kernels[5][2][2][2])(TcParams) = {
+      {{RC_TC_K(16, 4, 0), RC_TC_K(16, 4, 1)}, {RC_TC_K(16, 1, 0), RC_TC_K(16, 1, 1)}},
+      {{{nullptr, nullptr}, {nullptr, nullptr}}, {{nullptr, nullptr}, {nullptr, nullptr}}},
+      {{RC_TC_K(0, 4, 0), RC_TC_K(0, 4, 1)}, {RC_TC_K(0, 1, 0), RC_TC_K(0, 1, 1)}},
+      {{RC_TC_K(8, 4, 0), RC_TC_K(8, 4, 1)}, {RC_TC_K(8, 1, 0), RC_TC_K(8, 1, 1)}},
+      {{RC_TC_K(4, 4, 0), RC_TC_K(4, 4, 1)}, {RC_TC_K(4, 1, 0), RC_TC_K(4, 1, 1)}}};
+#undef RC_TC_K
   const int single = d.group == RC_GROUP_SINGLE, raw = d.convention == RC_CONV_RAW;
-  void (*fn)(TcParams) = kernels[gi][single][raw];
+  void (*fn)(TcParams) = kernels[gi][single][raw][passes == 3];
   RC_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)plan.bytes));
   const int grid = p.items < sms ? p.items : sms;
   prof_begin(s);
-  fn<<<grid, THREADS, plan.bytes, s>>>(p);
+  static const int threads_of[5] = {Epi<16>::THREADS, 0, Epi<0>::THREADS, Epi<8>::THREADS, Epi<4>::THREADS};
+  static const int budget_of[5] = {128 * Epi<16>::PROD + 32 * Epi<16>::WARPS * Epi<16>::REGS, 0,
+                                   128 * Epi<0>::PROD + 32 * Epi<0>::WARPS * Epi<0>::REGS,
+                                   128 * Epi<8>::PROD + 32 * Epi<8>::WARPS * Epi<8>::REGS,
+                                   128 * Epi<4>::PROD + 32 * Epi<4>::WARPS * Epi<4>::REGS};
+  cudaFuncAttributes fa;
+  RC_CUDA(cudaFuncGetAttributes(&fa, fn));
+  if (fa.numRegs * threads_of[gi] < budget_of[gi])  // setmaxnreg.inc would never be granted
+    return fail(RC_ERR_CUDA, "ri_conv: tensor-core kernel register budget exceeds its launch allocation");
+  fn<<<grid, threads_of[gi], plan.bytes, s>>>(p);
   prof_end(s);
   RC_CUDA(cudaGetLastError());
   return RC_OK;
@@ -969,7 +1261,7 @@ int launch_tc(const rc_desc& d, const float* x, const void* bank, const float* b
 extern "C" int rc_tc_prof(unsigned long long* host, int n, int reset) {
   if (host && n > 0) RC_CUDA(cudaMemcpyFromSymbol(host, g_tc_prof, sizeof(unsigned long long) * (size_t)n));
   if (reset) {
-    static unsigned long long zeros[1024 * 16];
+    static unsigned long long zeros[1024 * 32];
     RC_CUDA(cudaMemcpyToSymbol(g_tc_prof, zeros, sizeof(zeros)));
   }
   return RC_OK;

@@ -11,11 +11,12 @@ def test_smem_traffic_c3_geometry():
     import paper_2512_08888_b200 as P
     d = P.Desc(256, 256, 16, 16, 1024, 3, "steer", 8, "subgroup", 4, "scatter", "auto")
     b = bench.smem_traffic(d, "tc_k3w16_bf16x3")
-    # per item: bands N = 80, 96, 96, 80 (edge bands trimmed); K-step = 3*4096 + 3*N*32 + 2*4096
-    per_kstep = lambda n: 3 * 4096 + 3 * n * 32 + 2 * 4096
-    per_item = sum(2 * 9 * 4 * 4 * per_kstep(n) + 2 * 4 * n * 128 for n in (80, 96, 96, 80))
+    # carry bands: 4 bands x 2 bases of N = 64 px; K-step = Wh + Wl reads (2 x 4 KB), B rows
+    # 128 + 64 (x 32 B), TMA weight writes 2 x 4 KB; X (hi + lo) written once per unit
+    per_kstep = 2 * 4096 + 192 * 32 + 2 * 4096
+    per_item = 2 * 4 * (9 * 4 * 4 * per_kstep + 2 * 4 * 64 * 128)
     assert b == per_item * 256 * 8
-    assert 68e9 < b < 70e9
+    assert 53e9 < b < 55e9
     assert bench.smem_traffic(d, "simt_k3<8,2,4>") is None
     one = bench.smem_traffic(d, "tc_k3w16_bf16")
     assert one < b / 2  # one pass: 1 A + 1 B read and 1 weight part per K-step
@@ -29,7 +30,7 @@ def test_smem_roofline_fields():
         assert bench.smem_roofline(d, 2.35) is None or bench.smem_roofline(d, 2.35)["unit"] == "TB/s"
         return
     r = bench.smem_roofline(d, 2.35)
-    assert r["unit"] == "TB/s" and abs(r["peak"] - 37.2) < 0.1 and 0.7 < r["frac"] < 0.85
+    assert r["unit"] == "TB/s" and abs(r["peak"] - 37.2) < 0.1 and 0.5 < r["frac"] < 0.7
 
 
 def test_clock_sampler_unsampled_summary():

@@ -6,8 +6,8 @@ per CTA on average: each MMA warp's total / waiting-for-D / waiting-for-X / wait
 issuing cycles, the epilogue warp's total / waiting-for-D / finalize cycles and the
 producers' waits.  Experiment tooling; the shipped library has the counters compiled out.
 
-    python tools/tc_kernel_profile.py build            # here (nvcc cross-compiles)
-    python tools/tc_kernel_profile.py run N CIN H W COUT GROUP R POOL G [precision]
+    python tools/tc_kernel_profile.py build [VARIANT -DNAME=V ...]   # here (nvcc cross-compiles)
+    python tools/tc_kernel_profile.py run [--lib VARIANT] N CIN H W COUT GROUP R POOL G [precision]
 """
 import ctypes as C
 import os
@@ -17,30 +17,36 @@ import sys
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 VAR = os.path.join(ROOT, "tools", "variants")
-LIB = os.path.join(VAR, "librotconv_prof.so")
 NAMES = ["mma0 total", "mma0 wait D", "mma0 wait X", "mma0 wait W", "mma0 issue",
          "mma1 total", "mma1 wait D", "mma1 wait X", "mma1 wait W", "mma1 issue",
          "epi total", "epi wait Dfull", "epi finalize", "prod0 wait Wslot", "prod0 wait Xslot",
-         "prod1 wait Wslot"]
+         "prod1 wait Wslot", "epi8 total", "epi8 wait Dfull", "epi8 finalize"]
 
 
-def build():
+def lib_path(variant="prof"):
+    return os.path.join(VAR, f"librotconv_{variant}.so")
+
+
+def build(variant="prof", defines=()):
     from paper_2512_08888_b200 import build as B
     B.build()
     os.makedirs(VAR, exist_ok=True)
-    obj = os.path.join(VAR, "ri_tc_prof.o")
+    obj = os.path.join(VAR, f"ri_tc_{variant}.o")
     subprocess.check_call([B.NVCC, *B.ARCH, *[f for f in B.FLAGS if f not in ("-Xptxas", "-v")],
-                           "-DRC_TC_PROF=1", "-c", os.path.join(B.CSRC, "ri_tc.cu"), "-o", obj])
+                           "-DRC_TC_PROF=1", *defines, "-c", os.path.join(B.CSRC, "ri_tc.cu"), "-o", obj])
     objs = [os.path.join(B.BUILD, f) for f in sorted(os.listdir(B.BUILD))
             if f.endswith(".o") and f != "ri_tc.o"] + [obj]
-    subprocess.check_call([B.NVCC, *B.ARCH, "-shared", "-o", LIB, *objs, "-lcublas"])
-    print(LIB)
+    subprocess.check_call([B.NVCC, *B.ARCH, "-shared", "-o", lib_path(variant), *objs, "-lcublas"])
+    print(lib_path(variant))
 
 
 def run(a):
     import torch
     from paper_2512_08888_b200 import _lib
-    _lib.LIB_PATH = LIB
+    variant = "prof"
+    if a[0] == "--lib":
+        variant, a = a[1], a[2:]
+    _lib.LIB_PATH = lib_path(variant)
     _lib.SIGNATURES["rc_tc_prof"] = (C.c_int, [C.c_void_p, C.c_int, C.c_int])
     import paper_2512_08888_b200 as P
     n, cin, h, w, cout = map(int, a[:5])
@@ -63,13 +69,13 @@ def run(a):
         P.ri_conv_forward(desc, x, bank)
     a1.record()
     torch.cuda.synchronize()
-    buf = (C.c_ulonglong * (1024 * 16))()
-    L.rc_tc_prof(buf, 1024 * 16, 0)
+    buf = (C.c_ulonglong * (1024 * 32))()
+    L.rc_tc_prof(buf, 1024 * 32, 0)
     sms = torch.cuda.get_device_properties(0).multi_processor_count
     ctas = min(sms, (cout + 127) // 128 * n)
-    tot = [sum(buf[c * 16 + i] for c in range(ctas)) / ctas / reps for i in range(16)]
+    tot = [sum(buf[c * 32 + i] for c in range(ctas)) / ctas / reps for i in range(len(NAMES))]
     ms = a0.elapsed_time(a1) / reps
-    print(f"{desc.kernel_name()} {ms:.3f} ms per launch (incl. x_pack), {ctas} CTAs; per CTA per launch, "
+    print(f"[{variant}] {desc.kernel_name()} {ms:.3f} ms per launch (incl. x_pack), {ctas} CTAs; per CTA per launch, "
           f"Mcycles (share of the MMA warp 0 total):")
     for i, nm in enumerate(NAMES):
         print(f"  {nm:18s} {tot[i] / 1e6:8.3f}  {tot[i] / max(tot[0], 1):6.3f}")
@@ -77,6 +83,6 @@ def run(a):
 
 if __name__ == "__main__":
     if sys.argv[1] == "build":
-        build()
+        build(sys.argv[2] if len(sys.argv) > 2 else "prof", sys.argv[3:])
     else:
         run(sys.argv[2:])
