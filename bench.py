@@ -256,8 +256,9 @@ def smem_traffic(desc, kernel: str):
         N = 128 Wh x [Xh | Xl] MMA) + Wl once (Wl x Xh) and B = 128 + 64 rows x 32 B; bf16
         reads A once and B = 64 rows; the TMA writes parts x 4 KB of weights.  The X band
         (parts x NC x 64 px x 128 B) is written once per (base, band) unit.
-      * strips (tc_k3strip; 6x18 input px, N = 112): bf16x3 reads Ah twice + Al once and
-        Xh twice + Xl once; X written once per band (shared by the bases)."""
+      * strips of wider images (tc_k3strip): the same carry bands over 16-column strips, 4
+        input rows x 18 columns (halo columns only), N = 80; bf16x3 as three N = 80 MMAs (Ah
+        twice + Al once, Xh twice + Xl once); X written once per (base, band) unit."""
     if not (kernel.startswith("tc_k3w16") or kernel.startswith("tc_k3strip")):
         return None
     three = kernel.endswith("bf16x3")
@@ -273,8 +274,8 @@ def smem_traffic(desc, kernel: str):
     else:
         pa = 3 if three else 1
         bands = ((h + 3) // 4) * (w // 16)
-        kstep = pa * 4096 + pa * 112 * 32 + parts * 4096
-        per_item = bands * (NB * 9 * NC * 4 * kstep + parts * NC * 112 * 128)
+        kstep = pa * 4096 + pa * 80 * 32 + parts * 4096
+        per_item = NB * bands * (9 * NC * 4 * kstep + parts * NC * 80 * 128)
     return per_item * n * NCT
 
 

@@ -82,12 +82,12 @@ template <int TW>
 struct Geo {
   static constexpr bool STRIP = TW == 0;
   static constexpr bool SMALL = TW == 4 || TW == 8;
-  static constexpr bool CARRY = TW == 16;
-  static constexpr bool CAT = CARRY && RC_TC_CAT;             // bf16x3 as Wh x [Xh | Xl] + Wl x Xh
+  static constexpr bool CARRY = TW == 16 || TW == 0;          // rows carried across bands (no row halo)
+  static constexpr bool CAT = TW == 16 && RC_TC_CAT;          // bf16x3 as Wh x [Xh | Xl] + Wl x Xh
   static constexpr int OUT_ROWS = STRIP ? 4 : 64 / TW;        // 4 | 4 | 8 | 16
   static constexpr int IN_ROWS = (SMALL || CARRY) ? OUT_ROWS : OUT_ROWS + 2;
   static constexpr int RS = STRIP ? 18 : TW;                  // pixels per band row
-  static constexpr int BAND_PX = IN_ROWS * RS;                // 64 | 108 | 64 | 64
+  static constexpr int BAND_PX = IN_ROWS * RS;                // 64 | 72 | 64 | 64
   static constexpr int MMA_N = (BAND_PX + 15) / 16 * 16;
   static constexpr int XTILE = MMA_N * 64 * 2;                // bytes of one [MMA_N x 64 ci] bf16 tile
   // TMEM: columns [0, D0) hold the carried rows (CARRY: [0, 64) row 4k-1 of the band, [64,
@@ -114,9 +114,10 @@ constexpr int NUM_MMA = 2;               // MMA-issuing warps (1 and 2)
 // launch_tc checks it: 640 x 96 = 128 x 64 + 512 x 104;  384 x 168 = 128 x 56 + 256 x 224.
 template <int TW>
 struct Epi {
-  static constexpr int WARPS = TW == 16 ? 8 : 16;
-  static constexpr int REGS = TW == 16 ? 224 : 104;
-  static constexpr int PROD = TW == 16 ? 56 : 64;
+  static constexpr bool CARRY = Geo<TW>::CARRY;
+  static constexpr int WARPS = CARRY ? 8 : 16;
+  static constexpr int REGS = CARRY ? 224 : 104;
+  static constexpr int PROD = CARRY ? 56 : 64;
   static constexpr int THREADS = 32 * (EPI_WARP0 + WARPS);
 };
 constexpr int MAX_NDB = 6;
@@ -459,25 +460,31 @@ __device__ __forceinline__ void epi_tap(EpiState& e, float (&Y)[RPB][XH], uint64
 }
 
 // ---- 16-wide carry bands ---------------------------------------------------------------
-// D-row i of a CARRY D buffer (input row 4k + i): 16 columns of Z(Xh) (+ Z(Xl), bf16x3)
-template <bool cat>
+// D-row i of a CARRY D buffer (input row 4k + i): the thread's 16 columns of Z(Xh) (+ Z(Xl),
+// bf16x3 concatenation) into z[1..16]; strips also the halo columns 16j-1, 16j+16 (z[0], z[17])
+template <bool cat, int TW>
 __device__ __forceinline__ void load_row_cat(uint32_t a, float (&z)[18]) {
-  float(&zz)[16] = *reinterpret_cast<float(*)[16]>(&z[1]);
-  tmem_ld16(a, zz);
-  if constexpr (cat) {
-    float t[16];
-    tmem_ld16(a + Geo<16>::MMA_N, t);
+  if constexpr (TW == 0) {
+    issue_row<0>(a, z);
     tmem_wait_ld();
-#pragma unroll
-    for (int j = 0; j < 16; ++j) zz[j] += t[j];
   } else {
-    tmem_wait_ld();
+    float(&zz)[16] = *reinterpret_cast<float(*)[16]>(&z[1]);
+    tmem_ld16(a, zz);
+    if constexpr (cat) {
+      float t[16];
+      tmem_ld16(a + Geo<16>::MMA_N, t);
+      tmem_wait_ld();
+#pragma unroll
+      for (int j = 0; j < 16; ++j) zz[j] += t[j];
+    } else {
+      tmem_wait_ld();
+    }
   }
 }
 
 // scatter one input row into a row state kept in TMEM (carry + r*16 = rotation r, 16 px):
 // read-modify-write of each rotation that takes this row (I = 1 + di, as scatter_row)
-template <int RPB, int CONV, int T, int I>
+template <int RPB, int CONV, int T, int I, int TW>
 __device__ __forceinline__ void rmw_row(uint32_t carry, const float (&z)[18]) {
   bool wrote = false;
 #pragma unroll
@@ -491,7 +498,7 @@ __device__ __forceinline__ void rmw_row(uint32_t carry, const float (&z)[18]) {
 #pragma unroll
     for (int x = 0; x < 16; ++x) {
       const int src = x + dj + 1;
-      if (src < 1 || src > 16) continue;
+      if (TW == 16 && (src < 1 || src > 16)) continue;  // strips: z[0], z[17] are the halo columns
       c[x] += z[src];
     }
     tmem_st16(carry + r * 16, c);
@@ -508,11 +515,12 @@ __device__ __forceinline__ void rmw_row(uint32_t carry, const float (&z)[18]) {
 //          TMEM carry A = row 4k-1 (D-row 0; k > 0)
 // Each thread reads the 4 D-rows once per tap.  I = 1 + di selects the rotations of tap T
 // that read the row (scatter_row).
-template <int RPB, int CONV, int H, int T, bool cat>
+template <int TW, int RPB, int CONV, int H, int T, bool cat>
 __device__ __forceinline__ void epi_tap_carry(EpiState& e, float (&Y0)[RPB][XH], float (&Y1)[RPB][XH],
                                               bool first_band, uint32_t carry, uint64_t* d_full,
                                               uint64_t* d_empty) {
-  using G = Geo<16>;
+  using G = Geo<TW>;
+  constexpr uint32_t RS = G::RS;
   const uint32_t a = e.row_base + e.db * G::DCOLS;
   float z[18];
   PROF_T(t_df);
@@ -521,32 +529,32 @@ __device__ __forceinline__ void epi_tap_carry(EpiState& e, float (&Y0)[RPB][XH],
   if (threadIdx.x / 32 == EPI_WARP0 + 4) PROF_ADD(17, t_df);
   tc_fence_after();
   if constexpr (H == 0) {
-    load_row_cat<cat>(a, z);
-    scatter_row<16, RPB, CONV, T, 1>(Y0, z);
-    scatter_row<16, RPB, CONV, T, 0>(Y1, z);
-    load_row_cat<cat>(a + 16, z);
-    scatter_row<16, RPB, CONV, T, 2>(Y0, z);
-    scatter_row<16, RPB, CONV, T, 1>(Y1, z);
-    load_row_cat<cat>(a + 32, z);
-    scatter_row<16, RPB, CONV, T, 2>(Y1, z);
-    load_row_cat<cat>(a + 48, z);
+    load_row_cat<cat, TW>(a, z);
+    scatter_row<TW, RPB, CONV, T, 1>(Y0, z);
+    scatter_row<TW, RPB, CONV, T, 0>(Y1, z);
+    load_row_cat<cat, TW>(a + RS, z);
+    scatter_row<TW, RPB, CONV, T, 2>(Y0, z);
+    scatter_row<TW, RPB, CONV, T, 1>(Y1, z);
+    load_row_cat<cat, TW>(a + 2 * RS, z);
+    scatter_row<TW, RPB, CONV, T, 2>(Y1, z);
+    load_row_cat<cat, TW>(a + 3 * RS, z);
     release_d(e, G::NDB, d_empty);
-    rmw_row<RPB, CONV, T, 0>(carry, z);
+    rmw_row<RPB, CONV, T, 0, TW>(carry, z);
   } else {
-    load_row_cat<cat>(a + 16, z);
-    scatter_row<16, RPB, CONV, T, 0>(Y0, z);
-    load_row_cat<cat>(a + 32, z);
-    scatter_row<16, RPB, CONV, T, 1>(Y0, z);
-    scatter_row<16, RPB, CONV, T, 0>(Y1, z);
-    load_row_cat<cat>(a + 48, z);
-    scatter_row<16, RPB, CONV, T, 2>(Y0, z);
-    scatter_row<16, RPB, CONV, T, 1>(Y1, z);
+    load_row_cat<cat, TW>(a + RS, z);
+    scatter_row<TW, RPB, CONV, T, 0>(Y0, z);
+    load_row_cat<cat, TW>(a + 2 * RS, z);
+    scatter_row<TW, RPB, CONV, T, 1>(Y0, z);
+    scatter_row<TW, RPB, CONV, T, 0>(Y1, z);
+    load_row_cat<cat, TW>(a + 3 * RS, z);
+    scatter_row<TW, RPB, CONV, T, 2>(Y0, z);
+    scatter_row<TW, RPB, CONV, T, 1>(Y1, z);
     if (first_band) {
       release_d(e, G::NDB, d_empty);
     } else {
-      load_row_cat<cat>(a, z);
+      load_row_cat<cat, TW>(a, z);
       release_d(e, G::NDB, d_empty);
-      rmw_row<RPB, CONV, T, 2>(carry, z);
+      rmw_row<RPB, CONV, T, 2, TW>(carry, z);
     }
   }
 }
@@ -555,23 +563,23 @@ __device__ __forceinline__ void epi_tap_carry(EpiState& e, float (&Y0)[RPB][XH],
 // in chunks of 4 pixels
 // (the TMEM loads are warp-collective, .sync.aligned: every lane loads, only live lanes,
 // co < Cout, store)
-template <int RPB>
+template <int TW, int RPB>
 __device__ __forceinline__ void finalize_carried(const TcParams& p, uint32_t carry, int n, int co, int b, int row,
-                                                 bool live, float bz) {
+                                                 int x0, bool live, float bz) {
 #pragma unroll 1
   for (int c4 = 0; c4 < 4; ++c4) {
     float Yc[RPB][4];
 #pragma unroll
     for (int r = 0; r < RPB; ++r) tmem_ld4(carry + r * 16 + c4 * 4, Yc[r]);
     tmem_wait_ld();
-    if (live) finalize_row<16, RPB, 4>(p, Yc, n, co, b, row, c4 * 4, bz);
+    if (live) finalize_row<TW, RPB, 4>(p, Yc, n, co, b, row, x0 + c4 * 4, bz);
   }
 }
 
-template <int RPB, int CONV, int H, bool P3>
+template <int TW, int RPB, int CONV, int H, bool P3>
 __device__ __forceinline__ void epilogue_carry_half(const TcParams& p, uint32_t tmem, uint64_t* d_full,
                                                     uint64_t* d_empty) {
-  using G = Geo<16>;
+  using G = Geo<TW>;
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int q = warp % 4;
   const int co_l = q * 32 + lane;
@@ -579,6 +587,7 @@ __device__ __forceinline__ void epilogue_carry_half(const TcParams& p, uint32_t 
   const uint32_t carry = lanes + (H == 1 ? 0u : 64u);  // TMEM columns [0, 64): carry A, [64, 128): carry B
   constexpr bool cat = G::CAT && P3;
   EpiState e{lanes + G::D0, 0, 0, lane, 0};
+  const int nrb = G::STRIP ? (p.H + 3) / 4 : p.NBK;  // row bands (per strip)
   float Y0[RPB][XH], Y1[RPB][XH];
   PROF_T(t_epi0);
   for (int item = blockIdx.x; item < p.items; item += gridDim.x) {
@@ -586,9 +595,11 @@ __device__ __forceinline__ void epilogue_carry_half(const TcParams& p, uint32_t 
     const int co = ct * 128 + co_l;
     const bool live = co < p.Cout;
     const float bz = (live && p.bias) ? p.bias[co] : 0.f;
+    // units (base b, band kk): strips are strip-major, kk = j * nrb + k (k = row band)
     for (int b = 0; b < p.NB; ++b)
-      for (int k = 0; k < p.NBK; ++k) {
-        const bool first = k == 0, last = k == p.NBK - 1;
+      for (int kk = 0; kk < p.NBK; ++kk) {
+        const int k = G::STRIP ? kk % nrb : kk, x0 = G::STRIP ? (kk / nrb) * 16 : 0;
+        const bool first = k == 0, last = k == nrb - 1;
         if (H == 0 && !first) {  // row 4k: its input row 4k-1 was scattered in band k-1
 #pragma unroll
           for (int r = 0; r < RPB; ++r) tmem_ld16(carry + r * 16, Y0[r]);
@@ -608,15 +619,15 @@ __device__ __forceinline__ void epilogue_carry_half(const TcParams& p, uint32_t 
           for (int r = 0; r < RPB; ++r) tmem_st16_zero(carry + r * 16);
           tmem_wait_st();
         }
-        epi_tap_carry<RPB, CONV, H, 0, cat>(e, Y0, Y1, first, carry, d_full, d_empty);
-        epi_tap_carry<RPB, CONV, H, 1, cat>(e, Y0, Y1, first, carry, d_full, d_empty);
-        epi_tap_carry<RPB, CONV, H, 2, cat>(e, Y0, Y1, first, carry, d_full, d_empty);
-        epi_tap_carry<RPB, CONV, H, 3, cat>(e, Y0, Y1, first, carry, d_full, d_empty);
-        epi_tap_carry<RPB, CONV, H, 4, cat>(e, Y0, Y1, first, carry, d_full, d_empty);
-        epi_tap_carry<RPB, CONV, H, 5, cat>(e, Y0, Y1, first, carry, d_full, d_empty);
-        epi_tap_carry<RPB, CONV, H, 6, cat>(e, Y0, Y1, first, carry, d_full, d_empty);
-        epi_tap_carry<RPB, CONV, H, 7, cat>(e, Y0, Y1, first, carry, d_full, d_empty);
-        epi_tap_carry<RPB, CONV, H, 8, cat>(e, Y0, Y1, first, carry, d_full, d_empty);
+        epi_tap_carry<TW, RPB, CONV, H, 0, cat>(e, Y0, Y1, first, carry, d_full, d_empty);
+        epi_tap_carry<TW, RPB, CONV, H, 1, cat>(e, Y0, Y1, first, carry, d_full, d_empty);
+        epi_tap_carry<TW, RPB, CONV, H, 2, cat>(e, Y0, Y1, first, carry, d_full, d_empty);
+        epi_tap_carry<TW, RPB, CONV, H, 3, cat>(e, Y0, Y1, first, carry, d_full, d_empty);
+        epi_tap_carry<TW, RPB, CONV, H, 4, cat>(e, Y0, Y1, first, carry, d_full, d_empty);
+        epi_tap_carry<TW, RPB, CONV, H, 5, cat>(e, Y0, Y1, first, carry, d_full, d_empty);
+        epi_tap_carry<TW, RPB, CONV, H, 6, cat>(e, Y0, Y1, first, carry, d_full, d_empty);
+        epi_tap_carry<TW, RPB, CONV, H, 7, cat>(e, Y0, Y1, first, carry, d_full, d_empty);
+        epi_tap_carry<TW, RPB, CONV, H, 8, cat>(e, Y0, Y1, first, carry, d_full, d_empty);
         PROF_T(t_fin);
         // Rows to store: h = 0 rows 4k, 4k+1; h = 1 the carried row 4k-1 (k > 0), row 4k+2 and,
         // in the last band (input row 4k+4 is padding), row 4k+3 -- otherwise row 4k+3
@@ -625,7 +636,7 @@ __device__ __forceinline__ void epilogue_carry_half(const TcParams& p, uint32_t 
         // inlined copies would only evict the tap loop from the instruction cache.
         int nrows = 2;
         if constexpr (H == 1) {
-          if (!first && 4 * k - 1 < p.H) finalize_carried<RPB>(p, carry, n, co, b, 4 * k - 1, live, bz);
+          if (!first && 4 * k - 1 < p.H) finalize_carried<TW, RPB>(p, carry, n, co, b, 4 * k - 1, x0, live, bz);
           if (!last) {
 #pragma unroll
             for (int r = 0; r < RPB; ++r) tmem_st16(carry + r * 16, Y1[r]);
@@ -636,7 +647,7 @@ __device__ __forceinline__ void epilogue_carry_half(const TcParams& p, uint32_t 
 #pragma unroll 1
         for (int i = 0; i < nrows; ++i) {
           const int row = 4 * k + 2 * H + i;
-          if (live && row < p.H) finalize_row<16, RPB, XH>(p, Y0, n, co, b, row, 0, bz);
+          if (live && row < p.H) finalize_row<TW, RPB, XH>(p, Y0, n, co, b, row, x0, bz);
           if (i == 0) {
 #pragma unroll
             for (int r = 0; r < RPB; ++r)
@@ -654,12 +665,12 @@ __device__ __forceinline__ void epilogue_carry_half(const TcParams& p, uint32_t 
 
 // the 8 epilogue warps of a carry kernel: half h = (warp - 4) / 4 of its lane quadrant
 // (compile time below the dispatch: each half's band loop is straight-line code)
-template <int RPB, int CONV, bool P3>
+template <int TW, int RPB, int CONV, bool P3>
 __device__ __forceinline__ void epilogue_carry(const TcParams& p, uint32_t tmem, uint64_t* d_full, uint64_t* d_empty) {
   if ((threadIdx.x / 32 - EPI_WARP0) / 4 == 0)
-    epilogue_carry_half<RPB, CONV, 0, P3>(p, tmem, d_full, d_empty);
+    epilogue_carry_half<TW, RPB, CONV, 0, P3>(p, tmem, d_full, d_empty);
   else
-    epilogue_carry_half<RPB, CONV, 1, P3>(p, tmem, d_full, d_empty);
+    epilogue_carry_half<TW, RPB, CONV, 1, P3>(p, tmem, d_full, d_empty);
 }
 
 // Epilogue warp of the halo-band geometries: lane quadrant q (co = q*32 + lane); sub-tile
@@ -955,7 +966,7 @@ __global__ void __launch_bounds__(Epi<TW>::THREADS, 1) ri_tc_kernel(const __grid
     // ------------------------------------------------------------ epilogue
     asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(Epi<TW>::REGS));
     if constexpr (G::CARRY)
-      epilogue_carry<RPB, CONV, P3>(p, tmem, d_full, d_empty);
+      epilogue_carry<TW, RPB, CONV, P3>(p, tmem, d_full, d_empty);
     else
       epilogue<TW, RPB, CONV>(p, tmem, d_full, d_empty);
   }
@@ -991,9 +1002,12 @@ __global__ void x_pack_kernel(const float* __restrict__ x, uint8_t* __restrict__
       img = n * G::IMGS + px / (TW * TW);
       row = (px / TW) % TW;
       col = px % TW;
-    } else if constexpr (G::CARRY) {  // input rows [4k, 4k+4), no halo
-      row = k * G::OUT_ROWS + px / G::RS;
-      col = px % G::RS;
+    } else if constexpr (G::CARRY) {  // input rows [4k, 4k+4), no row halo; strips: the columns
+                                      // 16j-1 .. 16j+16 of strip j, bands strip-major
+      const int nrb = (H + 3) / 4;
+      const int kb = G::STRIP ? bk % nrb : bk, js = G::STRIP ? bk / nrb : 0;
+      row = kb * G::OUT_ROWS + px / G::RS;
+      col = G::STRIP ? js * 16 - 1 + px % G::RS : px % G::RS;
     } else {
       row = k * G::OUT_ROWS - 1 + px / G::RS;
       col = G::STRIP ? j * 16 - 1 + px % G::RS : px % G::RS;
