@@ -51,6 +51,16 @@ WORKLOADS = {
 }
 
 
+
+# Compute peaks MEASURED_PEAKS.json does not hold, measured on a B200 of this pool by
+# tools/peak_probe.cu (profiles/r02/peaks/peak_probe.jsonl): FP32 FMA on the CUDA cores (FFMA
+# and packed FFMA2 reach the same rate), tcgen05 kind::tf32 and kind::f16 issue-rate peaks
+# of an operand-resident MMA loop (M = 128, N = 256) at 1965 MHz.
+PEAKS_SRC = "tools/peak_probe.cu, profiles/r02/peaks/peak_probe.jsonl"
+FFMA_PEAK = 72.7
+PROBED_PEAKS = {"ffma_tflops": 71.75, "ffma2_tflops": 72.72, "tcgen05_tf32_tflops": 1115.0,
+                "tcgen05_bf16_loop_tflops": 2229.0, "source": PEAKS_SRC}
+
 def arith_dtype(kernel: str) -> str:
     """Arithmetic the timed kernel computes in (not a precision claim)."""
     if kernel.startswith("tc_") and kernel.endswith("bf16x3"):
@@ -499,11 +509,11 @@ def run_stack(args, wl):
             "layer_ms": [round(t, 4) for t, _ in layer_ms],
             "roofline": {"bound": "tensor" if top.kernel_name().startswith("tc_") else "fp32-simt",
                          "kernel": top.kernel_name(), "achieved": achieved,
-                         "peak": tpeak if top.kernel_name().startswith("tc_") else 74.4,
+                         "peak": tpeak if top.kernel_name().startswith("tc_") else FFMA_PEAK,
                          "unit": "TFLOP/s",
-                         "frac": achieved / (tpeak if top.kernel_name().startswith("tc_") else 74.4),
+                         "frac": achieved / (tpeak if top.kernel_name().startswith("tc_") else FFMA_PEAK),
                          "traffic": None,
-                         "peak_source": f"{src} bf16 dense (tc) / derived FP32 FFMA peak (simt)",
+                         "peak_source": f"{src} bf16 dense (tc) / measured FP32 FFMA peak (simt, {PEAKS_SRC})",
                          "note": "dominant layer of the stack, alg FLOPs / its CUDA-event time"},
             "clocks": clk.summary(),
             "e2e": {"value": eff_total / e2e_s.item() / 1e12, "unit": "TFLOP/s",
@@ -675,11 +685,12 @@ def main():
             "alg_tflops": achieved * 1.0, "eff_tflops_per_gpu": value / world,
             "per_rank_ms": per_rank_ms, "timing": "max over ranks of each rank's CUDA-event step time",
             "roofline": {"bound": "tensor" if tc else "fp32-simt", "kernel": desc.kernel_name(),
-                         "achieved": achieved, "peak": tpeak if tc else 74.4, "unit": "TFLOP/s",
-                         "frac": achieved / (tpeak if tc else 74.4), "traffic": traffic,
+                         "achieved": achieved, "peak": tpeak if tc else FFMA_PEAK, "unit": "TFLOP/s",
+                         "frac": achieved / (tpeak if tc else FFMA_PEAK), "traffic": traffic,
                          "kernel_ms": kernel_ms, "step_ms": ms,
                          "peak_source": (f"{src} dense bf16 (MEASURED_PEAKS.json)" if tc else
-                                         "derived FP32 FFMA peak 148 SM x 128 x 2 x 1.965 GHz"),
+                                         f"measured FP32 FFMA peak ({PEAKS_SRC})"),
+                         "other_measured_peaks": PROBED_PEAKS,
                          "mma_passes": passes,
                          "frac_of_pass_ceiling": achieved * passes / tpeak if tc else None,
                          "smem": smem_roofline(desc, kernel_ms),
