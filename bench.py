@@ -48,7 +48,13 @@ WORKLOADS = {
     "c5": (1024, 3, 64, 64, 10, 3, "stack", 8, "subgroup", 4,
            "C5: RI classifier stack 64x64x3, 3 blocks (RI steer R=8 subgroup-4 + conv + ReLU + "
            "maxpool), widths 64/128/256, GAP + linear head"),
+    # C2: the paper's Appendix-A grid, one step = every cell once (its largest cell is the
+    # tuple's shape, used for the CPU sample and the roofline)
+    "c2": (32, 256, 16, 16, 1024, 3, "single", 1, "none", 1,
+           "C2: single-orientation scatter conv grid, inputs 4x4/8x8/16x16 x Cin 4..256 x Cout "
+           "256/512/1024, batch 32 per cell (63 cells per step)"),
 }
+C2_SIZES, C2_CINS, C2_COUTS = (4, 8, 16), (4, 8, 16, 32, 64, 128, 256), (256, 512, 1024)
 
 
 
@@ -527,6 +533,191 @@ def run_stack(args, wl):
         dist.destroy_process_group()
 
 
+def run_grid(args, wl):
+    """C2: the Appendix-A grid (63 single-orientation layers, batch 32 each) as one step.
+
+    value = the grid's effective FLOPs / the step's device time, the step being every cell
+    once (inputs resident, outputs preallocated, L2 flushed between steps); per cell, the
+    device time of one launch (CUDA-graph replays) next to cuDNN FP32 (FMA-only) and TF32 on
+    the same tensors (context: the paper's appendix comparison).  Each rank runs the whole
+    grid on its own images (weak scaling)."""
+    import torch
+    import torch.distributed as dist
+    import torch.nn.functional as F
+    import paper_2512_08888_b200 as P
+    from paper_2512_08888_b200 import _lib
+
+    rank, world = int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1))
+    local = int(os.environ.get("LOCAL_RANK", 0))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        dist.init_process_group("nccl", device_id=dev)
+    n = wl[0]
+    gen = torch.Generator(device=dev).manual_seed(4321 + rank)
+    cells = []
+    for sz in C2_SIZES:
+        for cin in C2_CINS:
+            for cout in C2_COUTS:
+                d = P.Desc(n, cin, sz, sz, cout, 3, "single", 1, "none", 1, "scatter", args.precision)
+                x = (torch.rand((n, cin, sz, sz), generator=gen, device=dev) * 2 - 1).contiguous()
+                w0 = ((torch.rand((cout, cin, 3, 3), generator=gen, device=dev) * 2 - 1) / np.sqrt(cin * 9)).contiguous()
+                cells.append({"desc": d, "x": x, "w": w0, "bank": P.bank_precompute(d, w0),
+                              "y": torch.empty((n, cout, 1, sz, sz), device=dev), "size": sz, "cin": cin, "cout": cout})
+
+    def step():
+        for c in cells:
+            P.ri_conv_forward(c["desc"], c["x"], c["bank"], out=c["y"])
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    s0 = torch.cuda.Stream(dev)
+    s0.wait_stream(torch.cuda.current_stream(dev))
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.stream(s0):
+        step()
+        torch.cuda.synchronize()
+        with torch.cuda.graph(graph, stream=s0):
+            step()
+    torch.cuda.synchronize()
+    flush = torch.empty(512 * 1024 * 1024 // 4, device=dev)
+    stream = torch.cuda.current_stream(dev)
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        for i in range(args.steps):
+            flush.fill_(float(i))
+            ev[i][0].record(stream)
+            graph.replay()
+            ev[i][1].record(stream)
+        clk.sample()
+        torch.cuda.synchronize()
+    times = [a.elapsed_time(b) for a, b in ev]
+    tot = torch.tensor([sum(times)], dtype=torch.float64, device=dev)
+    per_rank = [tot.clone() for _ in range(world)]
+    if world > 1:
+        dist.all_gather(per_rank, tot)
+        dist.all_reduce(tot, op=dist.ReduceOp.MAX)
+    ms = tot.item() / args.steps
+    eff = sum(2.0 * n * c["size"] ** 2 * 9 * c["cin"] * c["cout"] for c in cells)
+    value = eff * world / (ms * 1e-3) / 1e12
+
+    def graph_ms(fn, reps=20):  # one call's device time: 5 calls per graph replay
+        s1 = torch.cuda.Stream(dev)
+        s1.wait_stream(torch.cuda.current_stream(dev))
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.stream(s1):
+            fn()
+            torch.cuda.synchronize()
+            with torch.cuda.graph(g, stream=s1):
+                for _ in range(5):
+                    fn()
+        torch.cuda.synchronize()
+        ts = []
+        for _ in range(reps):
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            g.replay()
+            b.record()
+            b.synchronize()
+            ts.append(a.elapsed_time(b) / 5)
+        return statistics.median(ts)
+
+    rows, wins = [], 0
+    if rank == 0 and not args.no_cudnn:
+        torch.backends.cudnn.benchmark = True
+        for c in cells:
+            d, x, w0, bank, y = c["desc"], c["x"], c["w"], c["bank"], c["y"]
+            wf = torch.flip(w0, dims=(2, 3)).contiguous()  # scatter_conv_multi == conv2d(X, flip W)
+            ours = graph_ms(lambda: P.ri_conv_forward(d, x, bank, out=y))
+            torch.backends.cudnn.allow_tf32 = False
+            ref = F.conv2d(x, wf, padding=1)
+            err = ((y[:, :, 0] - ref).abs().max() / ref.abs().max()).item()
+            fp32 = graph_ms(lambda: F.conv2d(x, wf, padding=1))
+            torch.backends.cudnn.allow_tf32 = True
+            tf32 = graph_ms(lambda: F.conv2d(x, wf, padding=1))
+            torch.backends.cudnn.allow_tf32 = False
+            wins += ours <= fp32
+            rows.append([c["size"], c["cin"], c["cout"], d.kernel_name(), round(ours, 5), round(fp32, 5),
+                         round(tf32, 5), round(fp32 / ours, 3), float(f"{err:.2e}")])
+    big = cells[-1]  # 16x16x256 -> 1024
+    L = _lib.lib()
+    L.rc_profile_enable(1)
+    for _ in range(5):
+        P.ri_conv_forward(big["desc"], big["x"], big["bank"], out=big["y"])
+    torch.cuda.synchronize()
+    L.rc_profile_enable(0)
+    kms = (C.c_float * 5)()
+    nk = L.rc_profile_collect(kms, 5)
+    kernel_ms = statistics.median(kms[:nk]) if nk > 0 else None
+    tpeak, hbm, src = peaks()
+    tc = big["desc"].kernel_name().startswith("tc_")
+    achieved = big["desc"].alg_flops() / (kernel_ms * 1e-3) / 1e12 if kernel_ms else None
+    # e2e: every cell through the C-ABI host entry (pinned buffers, H2D + D2H per cell)
+    hbuf = []
+    for c in cells:
+        d = c["desc"]
+        hbuf.append((d.c(), c["x"].cpu().pin_memory(), c["w"].cpu().pin_memory(),
+                     torch.empty(tuple(c["y"].shape), pin_memory=True)))
+    pp = lambda t: C.c_void_p(t.data_ptr()) if t is not None else None
+
+    def e2e_step():
+        for cd, hx, hw, hy in hbuf:
+            _lib.check(L.rc_ri_conv_forward_host(C.byref(cd), pp(hx), pp(hw), None, None, pp(hy), None, local))
+
+    e2e_step()
+    t0 = time.perf_counter()
+    for _ in range(max(1, args.e2e_steps)):
+        e2e_step()
+    e2e_s = torch.tensor([(time.perf_counter() - t0) / max(1, args.e2e_steps)], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(e2e_s, op=dist.ReduceOp.MAX)
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        threads = os.cpu_count() or 1
+        v, info = cpu_reference(wl, threads, target_s=8.0, kind="reference")
+        cpu = {"value": v, "unit": "TFLOP/s", "cores": info["cores"], "kind": info["kind"],
+               "sample": info["sample"] + " (the grid's largest cell, 16x16x256->1024)",
+               "ms_full_layer_extrapolated": info["ms_full_layer_extrapolated"]}
+    if rank == 0:
+        out = {
+            "metric": "RI-conv layer effective TFLOP/s", "value": value, "unit": "TFLOP/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "mixed: " + ", ".join(sorted({arith_dtype(c["desc"].kernel_name()) for c in cells})),
+            "data": "synthetic (uniform[-1,1) inputs, uniform/sqrt(Cin*K^2) weights, random init)",
+            "config": {"workload": wl[-1], "global_batch": n * world, "n_per_gpu": n, "cells": len(cells),
+                       "sizes": list(C2_SIZES), "c_in": list(C2_CINS), "c_out": list(C2_COUTS), "k": 3,
+                       "group": "single", "orientations": 1, "parallelism": f"replicas dp{world}"},
+            "precision": args.precision, "l2": "flushed between timed iterations (512 MB write)",
+            "per_rank_ms": [round(t.item() / args.steps, 4) for t in per_rank],
+            "timing": "max over ranks of each rank's CUDA-event time of one CUDA-graph replay of the grid",
+            "roofline": {"bound": "tensor" if tc else "fp32-simt", "kernel": big["desc"].kernel_name(),
+                         "cell": "16x16x256->1024", "achieved": achieved,
+                         "peak": tpeak if tc else FFMA_PEAK, "unit": "TFLOP/s",
+                         "frac": (achieved / (tpeak if tc else FFMA_PEAK)) if achieved else None,
+                         "kernel_ms": kernel_ms, "traffic": None,
+                         "peak_source": f"{src} dense bf16 (MEASURED_PEAKS.json)" if tc else PEAKS_SRC},
+            "clocks": clk.summary(),
+            "e2e": {"value": eff * world / e2e_s.item() / 1e12, "unit": "TFLOP/s",
+                    "h2d_bytes_per_step": int(sum(h[1].numel() * 4 + h[2].numel() * 4 for h in hbuf)),
+                    "d2h_bytes_per_step": int(sum(h[3].numel() * 4 for h in hbuf)),
+                    "ms_per_step": e2e_s.item() * 1e3, "path": "rc_ri_conv_forward_host per cell (C-ABI)"},
+            "gpu_launches": args.steps * sum(2 if c["desc"].kernel_name().startswith("tc_") else 1 for c in cells),
+            "cpu_baseline": cpu,
+            "cells_vs_cudnn": {"columns": ["size", "c_in", "c_out", "kernel", "ours_ms", "cudnn_fp32_ms",
+                                           "cudnn_tf32_ms", "speedup_vs_fp32", "err_vs_cudnn"],
+                               "rows": rows, "cells_at_or_above_cudnn_fp32": wins},
+        }
+        print(json.dumps(out), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -547,6 +738,8 @@ def main():
         return run_reference(args, wl)
     if args.workload == "c5":
         return run_stack(args, wl)
+    if args.workload == "c2":
+        return run_grid(args, wl)
 
     import torch
     import torch.distributed as dist

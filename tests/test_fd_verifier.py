@@ -39,22 +39,27 @@ def test_fd_linear_map_and_errors():
 
 
 CASES = [
-    # (n, cin, h, w, cout, group, R, pool, g, activation)
-    (1, 4, 6, 6, 4, "p4", 4, "avg", 4, "none"),
-    (1, 4, 6, 6, 4, "p4m", 8, "max", 8, "none"),
-    (2, 3, 5, 7, 6, "steer", 8, "subgroup", 4, "relu"),
-    (1, 5, 6, 6, 3, "single", 1, "none", 1, "none"),
+    # (n, cin, h, w, cout, group, R, pool, g, activation, precision, tol)
+    (1, 4, 6, 6, 4, "p4", 4, "avg", 4, "none", "fp32", 1e-5),
+    (1, 4, 6, 6, 4, "p4m", 8, "max", 8, "none", "fp32", 1e-5),
+    (2, 3, 5, 7, 6, "steer", 8, "subgroup", 4, "relu", "fp32", 1e-5),
+    (1, 5, 6, 6, 3, "single", 1, "none", 1, "none", "fp32", 1e-5),
+    # tensor-core geometries (16-wide carry bands, whole 8x8 images, implicit GEMM)
+    (1, 16, 5, 16, 8, "p4m", 8, "max", 8, "none", "bf16x3", 1e-4),
+    (1, 16, 8, 8, 8, "steer", 8, "subgroup", 4, "relu", "bf16x3", 1e-4),
+    (1, 16, 6, 16, 8, "p4", 4, "avg", 4, "none", "bf16x3", 1e-4),
+    (1, 16, 5, 12, 8, "single", 1, "none", 1, "none", "bf16x3", 1e-4),
 ]
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("precision,tol", [("fp32", 1e-5), ("bf16x3", 1e-4)])
-@pytest.mark.parametrize("case", CASES, ids=lambda c: "-".join(map(str, c)))
-def test_backward_vs_oracle_finite_differences(O, dev, case, precision, tol):
+@pytest.mark.parametrize("case", CASES, ids=lambda c: "-".join(map(str, c[:11])))
+def test_backward_vs_oracle_finite_differences(O, dev, case):
     import torch
     import paper_2512_08888_b200 as P
-    n, cin, h, w, cout, g, R, pool, pg, act = case
+    n, cin, h, w, cout, g, R, pool, pg, act, precision, tol = case
     desc = P.Desc(n, cin, h, w, cout, 3, g, R, pool, pg, "scatter", precision, act)
+    assert precision != "bf16x3" or desc.kernel_name().startswith("tc_"), desc.kernel_name()
     od = O.Desc(n, cin, h, w, cout, 3, g, R, pool, pg, "scatter")
     rng = np.random.default_rng(abs(hash(case)) % 2**31)
     x = rng.uniform(-1, 1, (n, cin, h, w)).astype(np.float32)
@@ -72,7 +77,8 @@ def test_backward_vs_oracle_finite_differences(O, dev, case, precision, tol):
 
     base = {"x": x.astype(np.float64), "w0": w0.astype(np.float64),
             "w1": w1.astype(np.float64) if w1 is not None else None, "bias": bias.astype(np.float64)}
-    mm = m.reshape((n, cout, -1, h, w)) if pool not in ("avg", "max") else m
+    # the oracle squeezes R' = 1 away for avg / max pooling (oracle.ri_forward)
+    mm = m.reshape((n, cout, h, w)) if pool in ("avg", "max") else m.reshape((n, cout, -1, h, w))
 
     def fwd(vals):
         yy, aa = O.ri_forward(od, vals["x"], vals["w0"], vals["w1"], vals["bias"])
@@ -112,5 +118,5 @@ def test_backward_vs_oracle_finite_differences(O, dev, case, precision, tol):
         gan = grads[name].double().cpu().numpy()
         err, used = fd.finite_diff_check(loss_of(name), base[name], gan, 1e-5, samples=50,
                                          seed=len(name), skip=skip_of(name))
-        assert used >= 30, (name, used)
+        assert used >= min(30, base[name].size // 2), (name, used)
         assert err <= tol, (name, err)

@@ -68,13 +68,26 @@ def rotated_kernels(P, desc, w0, w1):
     return P.rotconv.build_orientation_bank_from(desc, w0, w1)
 
 
-def run_cell(P, mode, size, cin, cout, args, gen):
+def cell_seed(args, size, cin, cout):
+    """Identical seeds per cell across modes."""
+    return args.seed + size * 7919 + cin * 31 + cout
+
+
+def cell_tensors(size, cin, cout, args, gen):
+    """The cell's seeded inputs X (n, cin, size, size) and kernels W0, W1 (cout, cin, k, k)."""
     dev = torch.device("cuda")
-    n, k, R = args.batch, args.kernel, args.orientations
+    n, k = args.batch, args.kernel
     x = (torch.rand((n, cin, size, size), generator=gen, device=dev) * 2 - 1).contiguous()
     s = 1 / math.sqrt(cin * k * k)
     w0 = ((torch.rand((cout, cin, k, k), generator=gen, device=dev) * 2 - 1) * s).contiguous()
     w1 = ((torch.rand((cout, cin, k, k), generator=gen, device=dev) * 2 - 1) * s).contiguous()
+    return x, w0, w1
+
+
+def run_cell(P, mode, size, cin, cout, args, gen):
+    dev = torch.device("cuda")
+    n, k, R = args.batch, args.kernel, args.orientations
+    x, w0, w1 = cell_tensors(size, cin, cout, args, gen)
     base_mults = n * size * size * k * k * cin * cout
     if mode in ("scatter", "gather", "im2col_matmul"):
         desc = P.Desc(n, cin, size, size, cout, k, "single", 1, "none", 1, "scatter", args.precision)
@@ -111,7 +124,7 @@ def run_cell(P, mode, size, cin, cout, args, gen):
     return base_mults * R, 0, err, (lambda: F.conv2d(x, wcat, padding=k // 2)), R
 
 
-def main():
+def parse_args(argv=None):
     ap = argparse.ArgumentParser(description=__doc__.split("\n")[0])
     ap.add_argument("--sizes", type=int, nargs="+", default=[8, 16, 32])
     ap.add_argument("--cin", type=int, nargs="+", default=[64, 256])
@@ -129,7 +142,11 @@ def main():
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--out", default=None)
     ap.add_argument("--format", default="csv", choices=["csv", "md"])
-    args = ap.parse_args()
+    return ap.parse_args(argv)
+
+
+def main(argv=None):
+    args = parse_args(argv)
     import paper_2512_08888_b200 as P
     torch.backends.cudnn.benchmark = True
     torch.backends.cudnn.allow_tf32 = False
@@ -142,7 +159,7 @@ def main():
                     if args.kernel > size:
                         print(f"skip {mode} {size}x{size}: kernel > input", file=sys.stderr)
                         continue
-                    gen = torch.Generator(device="cuda").manual_seed(args.seed + size * 7919 + cin * 31 + cout)
+                    gen = torch.Generator(device="cuda").manual_seed(cell_seed(args, size, cin, cout))
                     mults, aux, err, fn, R = run_cell(P, mode, size, cin, cout, args, gen)
                     if not err <= 1e-4:
                         failed += 1
