@@ -193,8 +193,11 @@ struct DeviceGuard {
 int dispatch(const rc_desc& d, const float* x, const void* bank, const float* bias, float* y,
              uint8_t* am, void* ws, size_t ws_bytes, cudaStream_t s, bool dry, const char** name) {
   // AUTO keeps tiny channel counts on the CUDA cores: the tensor-core K chunk is 64 input
-  // channels, so Cin < 16 would multiply mostly zero padding (e.g. an RGB first layer).
-  const bool auto_tc = d.precision == RC_PREC_AUTO && d.c_in >= 16;
+  // channels, so Cin < 16 would multiply mostly zero padding (e.g. an RGB first layer); small
+  // single-orientation layers (Cin <= 8 on <= 32-wide images) run the direct FP32 kernel
+  // (at Cin = 16 the tensor-core kernels are faster, profiles/r02/c2/).
+  const bool small_direct = d.c_in <= 8 && direct_supported(d);
+  const bool auto_tc = d.precision == RC_PREC_AUTO && d.c_in >= 16 && !small_direct;
   if (d.precision == RC_PREC_BF16X3 || d.precision == RC_PREC_BF16 || auto_tc) {
     int st = launch_tc(d, x, bank, bias, y, am, ws, ws_bytes, s, dry, name);
     if (st != RC_ERR_UNSUPPORTED || d.precision != RC_PREC_AUTO) {
@@ -203,7 +206,11 @@ int dispatch(const rc_desc& d, const float* x, const void* bank, const float* bi
       return st;
     }
   }
-  int st = launch_simt_k3(d, x, bank, bias, y, am, s, dry, name);
+  // small single-orientation layers (Cin <= 16, W in {4, 8, 16, 32}): direct FP32 kernel
+  int st = d.precision == RC_PREC_FP32 || small_direct ? launch_direct_k3(d, x, bank, bias, y, am, s, dry, name)
+                                                       : RC_ERR_UNSUPPORTED;
+  if (st != RC_ERR_UNSUPPORTED) return st;
+  st = launch_simt_k3(d, x, bank, bias, y, am, s, dry, name);
   if (st != RC_ERR_UNSUPPORTED) return st;
   if (dry) {
     if (name) *name = "generic";

@@ -73,6 +73,10 @@ int launch_steer(const float* fx, const float* fy, size_t count, double theta, f
 // returns RC_ERR_UNSUPPORTED if the SIMT K=3 fast kernel cannot handle d
 int launch_simt_k3(const rc_desc& d, const float* x, const void* bank, const float* bias,
                    float* y, uint8_t* argmax, cudaStream_t s, bool dry_run, const char** name);
+// single-orientation K = 3, Cin <= 32, W in {4, 8, 16, 32} (ri_direct.cu); else RC_ERR_UNSUPPORTED
+bool direct_supported(const rc_desc& d);
+int launch_direct_k3(const rc_desc& d, const float* x, const void* bank, const float* bias, float* y,
+                     uint8_t* am, cudaStream_t s, bool dry_run, const char** name);
 int launch_generic(const rc_desc& d, const float* x, const void* bank, const float* bias,
                    float* y, uint8_t* argmax, cudaStream_t s, const char** name);
 int launch_pool(int n, int c_out, int r, int h, int w, int pool, int g, const float* f,
