@@ -194,9 +194,10 @@ int dispatch(const rc_desc& d, const float* x, const void* bank, const float* bi
              uint8_t* am, void* ws, size_t ws_bytes, cudaStream_t s, bool dry, const char** name) {
   // AUTO keeps tiny channel counts on the CUDA cores: the tensor-core K chunk is 64 input
   // channels, so Cin < 16 would multiply mostly zero padding (e.g. an RGB first layer); small
-  // single-orientation layers (Cin <= 8 on <= 32-wide images) run the direct FP32 kernel
-  // (at Cin = 16 the tensor-core kernels are faster, profiles/r02/c2/).
-  const bool small_direct = d.c_in <= 8 && direct_supported(d);
+  // single-orientation layers (Cin <= 8 on <= 32-wide images, Cin <= 16 on 4x4 images) run
+  // the direct FP32 kernel (elsewhere at Cin = 16 the tensor-core kernels are faster,
+  // profiles/r02/c2/).
+  const bool small_direct = (d.c_in <= 8 || (d.c_in <= 16 && d.w == 4)) && direct_supported(d);
   const bool auto_tc = d.precision == RC_PREC_AUTO && d.c_in >= 16 && !small_direct;
   if (d.precision == RC_PREC_BF16X3 || d.precision == RC_PREC_BF16 || auto_tc) {
     int st = launch_tc(d, x, bank, bias, y, am, ws, ws_bytes, s, dry, name);

@@ -19,6 +19,11 @@
 namespace rc {
 namespace {
 
+__device__ __forceinline__ void cp_async4(float* smem, const float* gmem, bool valid) {
+  const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;\n" ::"r"(d), "l"(gmem), "r"(valid ? 4 : 0));
+}
+
 constexpr int DCO = 32;      // output channels per CTA (one per lane)
 constexpr int WS = DCO + 1;  // weight row stride in shared memory (conflict-free transposed fill)
 constexpr int DMAX_CIN = 32;
@@ -42,43 +47,28 @@ __global__ void __launch_bounds__(32 * RW) direct_k3_kernel(const __grid_constan
   const int co0 = blockIdx.x * DCO, co = co0 + lane;
   // weights of the CTA's 32 channels: coalesced reads of [co][ci][t], transposed into
   // [ci * 9 + t][lane] rows of stride 33 (conflict-free both ways)
-  // (both fills issue LB global loads before their shared-memory stores: the whole layer is
-  // a few microseconds, so serialised load latencies would dominate it)
-  constexpr int LB = 8;
+  // Both fills are cp.async copies (4 bytes, zero-filled outside the image / channel range):
+  // no thread waits on one load before issuing the next -- the whole layer is a few
+  // microseconds, so serialised load latencies would dominate it.
   const int taps = p.Cin * 9;
-  for (int i0 = threadIdx.x; i0 < taps * DCO; i0 += LB * blockDim.x) {
-    float v[LB];
-#pragma unroll
-    for (int u = 0; u < LB; ++u) {
-      const int i = i0 + u * blockDim.x, l = i / taps;
-      v[u] = (i < taps * DCO && co0 + l < p.Cout) ? p.w[(size_t)co0 * taps + i] : 0.f;
-    }
-#pragma unroll
-    for (int u = 0; u < LB; ++u) {
-      const int i = i0 + u * blockDim.x, l = i / taps;
-      if (i < taps * DCO) ws[(i - l * taps) * WS + l] = v[u];
-    }
+  for (int i = threadIdx.x; i < taps * DCO; i += blockDim.x) {
+    const int l = i / taps;
+    const bool ok = co0 + l < p.Cout;
+    cp_async4(&ws[(i - l * taps) * WS + l], ok ? p.w + (size_t)co0 * taps + i : p.w, ok);
   }
   const int unit = blockIdx.y * RW + warp;  // (image, row group) of this warp
   const bool live = unit < p.units;
   const int n = live ? unit / p.row_groups : 0, r0 = live ? (unit % p.row_groups) * TR : 0;
   if (live) {
     const float* xn = p.x + (size_t)n * p.Cin * p.H * W;
-    const int total = p.Cin * PR * PW;
-    for (int i0 = lane; i0 < total; i0 += LB * 32) {
-      float v[LB];
-#pragma unroll
-      for (int u = 0; u < LB; ++u) {
-        const int i = i0 + u * 32;
-        const int c = i % PW, r = (i / PW) % PR, ci = i / (PW * PR);
-        const int hh = r0 - 1 + r, ww = c - 1;
-        v[u] = (i < total && hh >= 0 && hh < p.H && ww >= 0 && ww < W) ? xn[((size_t)ci * p.H + hh) * W + ww] : 0.f;
-      }
-#pragma unroll
-      for (int u = 0; u < LB; ++u)
-        if (i0 + u * 32 < total) xs[i0 + u * 32] = v[u];
+    for (int i = lane; i < p.Cin * PR * PW; i += 32) {
+      const int c = i % PW, r = (i / PW) % PR, ci = i / (PW * PR);
+      const int hh = r0 - 1 + r, ww = c - 1;
+      const bool ok = hh >= 0 && hh < p.H && ww >= 0 && ww < W;
+      cp_async4(&xs[i], ok ? xn + ((size_t)ci * p.H + hh) * W + ww : xn, ok);
     }
   }
+  asm volatile("cp.async.wait_all;\n" ::: "memory");
   __syncthreads();
   if (!live) return;
   float acc[TR][W];
