@@ -56,6 +56,41 @@ __global__ void bank_kernel(const float* __restrict__ w0, const float* __restric
   }
 }
 
+// K == 3: one CTA per (base b, 32 output channels, 32 input channels), staged through shared
+// memory so both HBM sides are coalesced: the [co][ci][9] rows of the weights and of the
+// FilterBank-layout bases are contiguous 32 x 9-float runs per channel, and the SIMT operand
+// [B][Cin][Cout][12] is written as contiguous 32 x 12-float runs per input channel (the
+// per-thread kernel above reads and writes 36-byte pieces strided by Cin x 9 floats).
+constexpr int BT = 32;
+__global__ void __launch_bounds__(256) bank_k3_tiled_kernel(const float* __restrict__ w0, const float* __restrict__ w1,
+                                                            float* __restrict__ bases, float* __restrict__ simt,
+                                                            int cout, int cin, int group, SteerCoeffs co_) {
+  __shared__ float tile[BT][BT * 9 + 1];  // [co_l][ci_l * 9 + t]
+  const int b = blockIdx.z, co0 = blockIdx.y * BT, ci0 = blockIdx.x * BT;
+  const int nco = min(BT, cout - co0), nci = min(BT, cin - ci0);
+  for (int e = threadIdx.x; e < BT * BT * 9; e += blockDim.x) {
+    const int col = e / (BT * 9), rem = e % (BT * 9), cil = rem / 9, t = rem % 9;
+    if (col >= nco || cil >= nci) continue;
+    const size_t src = ((size_t)(co0 + col) * cin + ci0 + cil) * 9;
+    float val;
+    if (group == RC_GROUP_STEER)  // SPEC:439-447, each op rounded (bit-identical to rco_steer)
+      val = __fadd_rn(__fmul_rn(co_.s[b], w0[src + t]), __fmul_rn(co_.c[b], w1[src + t]));
+    else if (group == RC_GROUP_P4M && b == 1)
+      val = w0[src + (t / 3) * 3 + (2 - t % 3)];  // tensor.hpp:363-370 mirror_plane
+    else
+      val = w0[src + t];
+    tile[col][rem] = val;
+    bases[((size_t)b * cout + co0 + col) * cin * 9 + (size_t)(ci0 + cil) * 9 + t] = val;
+  }
+  if (simt == nullptr) return;
+  __syncthreads();
+  for (int e = threadIdx.x; e < BT * BT * 12; e += blockDim.x) {
+    const int cil = e / (BT * 12), rem = e % (BT * 12), col = rem / 12, j = rem % 12;
+    if (col >= nco || cil >= nci) continue;
+    simt[(((size_t)b * cin + ci0 + cil) * cout + co0 + col) * 12 + j] = j < 9 ? tile[col][cil * 9 + j] : 0.f;
+  }
+}
+
 struct RotMaps {
   int8_t src[4][kMaxK * kMaxK];
 };
@@ -105,9 +140,16 @@ int launch_bank(const rc_desc& d, const float* w0, const float* w1, void* bank, 
   float* simt = L.simt_bytes ? reinterpret_cast<float*>(base + L.simt_off) : nullptr;
   const long long work = (long long)nb * d.c_in * d.c_out;
   if (work == 0) return RC_OK;
-  bank_kernel<<<grid_for(work, 256), 256, 0, s>>>(
-      w0, d.group == RC_GROUP_STEER ? w1 : w0, reinterpret_cast<float*>(base + L.bases_off), simt,
-      nb, d.c_out, d.c_in, d.k, d.group, c);
+  if (d.k == 3) {
+    const dim3 grid((d.c_in + BT - 1) / BT, (d.c_out + BT - 1) / BT, nb);
+    bank_k3_tiled_kernel<<<grid, 256, 0, s>>>(w0, d.group == RC_GROUP_STEER ? w1 : w0,
+                                               reinterpret_cast<float*>(base + L.bases_off), simt, d.c_out, d.c_in,
+                                               d.group, c);
+  } else {
+    bank_kernel<<<grid_for(work, 256), 256, 0, s>>>(
+        w0, d.group == RC_GROUP_STEER ? w1 : w0, reinterpret_cast<float*>(base + L.bases_off), simt,
+        nb, d.c_out, d.c_in, d.k, d.group, c);
+  }
   RC_CUDA(cudaGetLastError());
   if (L.tc_bytes)  // tcgen05 operand tiles (bf16 hi/lo, SW128) from the fp32 bases
     return launch_tc_wpack(d, reinterpret_cast<const float*>(base + L.bases_off),
