@@ -273,7 +273,7 @@ def smem_traffic(desc, kernel: str):
         reads A once and B = 64 rows; the TMA writes parts x 4 KB of weights.  The X band
         (parts x NC x 64 px x 128 B) is written once per (base, band) unit.
       * strips of wider images (tc_k3strip): the same carry bands over 16-column strips, 4
-        input rows x 18 columns (halo columns only), N = 80; bf16x3 as three N = 80 MMAs (Ah
+        input rows x 18 columns (halo columns only), N = 72; bf16x3 as three N = 72 MMAs (Ah
         twice + Al once, Xh twice + Xl once); X written once per (base, band) unit."""
     if not (kernel.startswith("tc_k3w16") or kernel.startswith("tc_k3strip")):
         return None
@@ -290,8 +290,8 @@ def smem_traffic(desc, kernel: str):
     else:
         pa = 3 if three else 1
         bands = ((h + 3) // 4) * (w // 16)
-        kstep = pa * 4096 + pa * 80 * 32 + parts * 4096
-        per_item = NB * bands * (9 * NC * 4 * kstep + parts * NC * 80 * 128)
+        kstep = pa * 4096 + pa * 72 * 32 + parts * 4096
+        per_item = NB * bands * (9 * NC * 4 * kstep + parts * NC * 72 * 128)
     return per_item * n * NCT
 
 

@@ -88,7 +88,7 @@ struct Geo {
   static constexpr int IN_ROWS = (SMALL || CARRY) ? OUT_ROWS : OUT_ROWS + 2;
   static constexpr int RS = STRIP ? 18 : TW;                  // pixels per band row
   static constexpr int BAND_PX = IN_ROWS * RS;                // 64 | 72 | 64 | 64
-  static constexpr int MMA_N = (BAND_PX + 15) / 16 * 16;
+  static constexpr int MMA_N = STRIP ? (BAND_PX + 7) / 8 * 8 : (BAND_PX + 15) / 16 * 16;  // strips: N = 72
   static constexpr int XTILE = MMA_N * 64 * 2;                // bytes of one [MMA_N x 64 ci] bf16 tile
   // TMEM: columns [0, D0) hold the carried rows (CARRY: [0, 64) row 4k-1 of the band, [64,
   // 128) row 4k+4) or keep the 1-column-left halo load of a band's first pixel inside the
