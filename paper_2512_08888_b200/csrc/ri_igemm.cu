@@ -331,6 +331,12 @@ IgGeom ig_geom(const rc_desc& d) {
   g.NCTW = (d.c_out + 127) / 128;
   g.NN = d.c_out >= 256 ? 256 : (d.c_out + 31) / 32 * 32;
   g.NCTN = (d.c_out + g.NN - 1) / g.NN;
+  // small layers: 128-channel N tiles when 256-channel tiles would leave SMs idle (the C2
+  // appendix cells: 81 pixel tiles at 16x16, N = 32)
+  if (g.NN == 256 && (long long)g.tiles * g.NCTN < 148) {
+    g.NN = 128;
+    g.NCTN = (d.c_out + 127) / 128;
+  }
   return g;
 }
 
