@@ -1013,8 +1013,12 @@ __global__ void x_pack_kernel(const float* __restrict__ x, uint8_t* __restrict__
       col = G::STRIP ? j * 16 - 1 + px % G::RS : px % G::RS;
     }
     const bool in = px < G::BAND_PX && ci < Cin && img < Nimg && row >= 0 && row < H && col >= 0 && col < W;
-    tile[cl][px] = in ? x[(((size_t)img * Cin + ci) * H + row) * W + col] : 0.f;
+    // cp.async (zero-filled outside): no thread waits on one load before issuing the next
+    const float* src = in ? x + (((size_t)img * Cin + ci) * H + row) * W + col : x;
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;\n" ::"r"(smem_u32(&tile[cl][px])), "l"(src),
+                 "r"(in ? 4 : 0));
   }
+  asm volatile("cp.async.wait_all;\n" ::: "memory");
   __syncthreads();
   const size_t tidx = ((size_t)n * NBK + bk) * NC + c;
   // CARRY: one tile per chunk of [MMA_N hi rows | MMA_N lo rows] (the N = 128 B operand of
