@@ -1,6 +1,6 @@
 """Small launches of every product kernel family for compute-sanitizer (memcheck / racecheck /
-synccheck): the tcgen05 band kernel (w16 bands, strips, 8x8 / 4x4 images, streamed X), the
-implicit GEMM, the FP32 CUDA-core kernels, the generic kernel, and the backward (pool / input /
+synccheck): the tcgen05 band kernel (carry bands on 16-wide images and strips, 8x8 / 4x4 images,
+streamed X), the implicit GEMM, the direct small-Cin kernel, the FP32 CUDA-core kernels, the generic kernel, and the backward (pool / input /
 tcgen05 weight gradient).  Prints one line per case; exits non-zero on a CUDA error.
 
     compute-sanitizer --tool memcheck python tools/sanitize_cases.py
@@ -21,6 +21,7 @@ CASES = [
     (5, 32, 4, 4, 128, "p4m", 8, "subgroup", 4, "bf16x3"),       # 4x4 images, ragged group
     (1, 576, 6, 32, 130, "p4", 4, "max", 4, "bf16x3"),           # streamed X (Cin > 512)
     (2, 64, 12, 20, 96, "single", 1, "none", 1, "bf16x3"),       # implicit GEMM
+    (4, 6, 8, 8, 40, "single", 1, "max", 1, "auto"),              # direct FP32 small-Cin kernel
     (2, 5, 16, 16, 7, "steer", 8, "subgroup", 4, "fp32"),        # SIMT FP32
     (2, 3, 7, 5, 4, "p4", 4, "max", 4, "fp32"),                  # generic (K = 5 below)
 ]
