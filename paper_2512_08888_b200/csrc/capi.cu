@@ -435,8 +435,10 @@ int rc_ri_conv_forward_host(const rc_desc* d, const float* h_x, const float* h_w
   }
   // Chunked pipeline over images: H2D of chunk i+1 and D2H of chunk i-1 overlap the kernels
   // of chunk i (three streams, the copies on the two copy engines).  Chunks of >= 16 images
-  // keep every copy large; small batches run as one chunk.
-  const int chunks = d->n >= 64 ? 8 : (d->n >= 32 ? 4 : 1);
+  // keep every copy large; small batches run as one chunk.  The output (D2H) dominates, so
+  // the sooner the first chunk is computed the sooner the D2H engine starts: 16 chunks from
+  // 256 images on.
+  const int chunks = d->n >= 256 ? 16 : (d->n >= 64 ? 8 : (d->n >= 32 ? 4 : 1));
   st = c.ensure_pipeline(2 * (size_t)chunks);
   if (st != RC_OK) {
     cudaStreamSynchronize(s);  // the bank upload / precompute may still read the caller's weights
