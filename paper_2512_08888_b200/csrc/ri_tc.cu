@@ -782,7 +782,10 @@ __global__ void __launch_bounds__(Epi<TW>::THREADS, 1) ri_tc_kernel(const __grid
   const int stage_w = p.spc * parts * WTILE;                      // W bytes of a stage
   const int stage_bytes = stage_w + (p.xstream ? p.spc * parts * XS : 0);
   const int stages_per_tap = p.NC / p.spc;
-  const int S0 = (S + 1) / 2;  // ring 0 (MMA warp 1): slots [0, S0); ring 1 (MMA warp 2): [S0, S)
+  // ring 0 (MMA warp 1): slots [0, S0); ring 1 (MMA warp 2): [S0, S).  The odd slot goes to ring 1:
+  // producer 0 also loads the X bands, so ring 0 runs fuller anyway (C3 -1.3%, C4 -2.5%,
+  // profiles/r02/c3_carry/variants_ab.txt)
+  const int S0 = S / 2;
   // X chunk c of a region of `cnt` chunks (the resident band: NC; a streamed stage: spc).
   // CARRY: [Xh rows | Xl rows] of a chunk are adjacent (one N = 128 B operand, one copy);
   // otherwise [hi chunks][lo chunks].
